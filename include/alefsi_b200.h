@@ -1,0 +1,157 @@
+/*
+ * alefsi_b200 — C ABI of the B200-native linear-solve path of the
+ * approximated-Newton ALE-FSI solver (arXiv 1904.02401).
+ *
+ * This is the boundary a Python ctypes binding of the reference package
+ * (pkg/src/alefsi) uses to replace its CPU solver objects; see
+ * INTEGRATION.md for the binding.  Every entry point returns 0 on success or
+ * an ALEFSI_ERR_* code; alefsi_last_error() describes the failure.
+ * Plain pointers and sizes only.  Unless stated otherwise vector arguments
+ * of the alefsi_mg_* calls are DEVICE pointers enqueued on the handle's
+ * stream; functions with a host_ptrs flag accept host buffers when it is 1
+ * and then synchronise before returning.
+ *
+ * Index conventions follow the reference: a level's dofs are node-major,
+ * dof = node * nc + component with nc = dim + 1 (p, v_1..v_d); level 0 is
+ * the coarsest level.
+ */
+#ifndef ALEFSI_B200_H
+#define ALEFSI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ALEFSI_OK 0
+#define ALEFSI_ERR_ARG 1
+#define ALEFSI_ERR_CUDA 2
+#define ALEFSI_ERR_SINGULAR 3       /* linsolve.py:132-133 "singular Vanka patch block" */
+#define ALEFSI_ERR_NOT_CONVERGED 4  /* linsolve.py:110-114 GMRES stalled -> SolverError */
+#define ALEFSI_ERR_STATE 5
+#define ALEFSI_ERR_INTERNAL 6
+
+typedef struct alefsi_mg_opaque* alefsi_mg;
+
+const char* alefsi_last_error(void);
+int alefsi_abi_version(void);
+int alefsi_device_count(int32_t* count);
+
+/* ---- host-side index structures (no GPU needed) ------------------------ */
+
+/* Row-sorted union of element stencils; replaces BlockPattern's key
+ * construction (reference fem.py:119-133).  Call once with indices == NULL
+ * to fill indptr[n_nodes+1], then again with indices[indptr[n_nodes]]. */
+int alefsi_pattern_build(int64_t n_nodes, int64_t n_elem, const int64_t* elem_ptr,
+                         const int64_t* elem_nodes, int64_t* indptr, int32_t* indices);
+
+/* slots[e][a][b] of the pair (elem[e][a], elem[e][b]) or -1; replaces
+ * BlockPattern.slots_for (reference fem.py:138-146). */
+int alefsi_pattern_slots(int64_t n_nodes, const int64_t* indptr, const int32_t* indices,
+                         int64_t n_elem, int32_t npe, const int64_t* elem_nodes, int64_t* slots);
+
+/* data[slot(e,a,b)] += local[e][a][b] (bs doubles per pair) in flattened
+ * order; replaces BlockPattern.scatter / scatter_subset np.add.at
+ * (reference fem.py:151-155, 166-169). */
+int alefsi_scatter_add_blocks(int64_t n_nodes, const int64_t* indptr, const int32_t* indices,
+                              int64_t n_elem, int32_t npe, const int64_t* elem_nodes, int32_t bs,
+                              const double* local, double* data, int32_t skip_missing);
+
+/* Greedy first-fit patch coloring; replaces color_patches
+ * (reference mesh.py:522-556).  patch_size is the dof count per patch. */
+int alefsi_color_patches(int64_t n_patches, const int64_t* patch_ptr, const int64_t* patch_nodes,
+                         const int64_t* patch_size, int64_t n_nodes, int64_t* color,
+                         int64_t* n_colors);
+
+/* ---- device multigrid hierarchy ----------------------------------------- */
+
+/* MgSolver(levels, nu_pre, nu_post) + VankaSmoother(omega)
+ * (reference linsolve.py:229-236, 147-161). */
+int alefsi_mg_create(int32_t n_levels, int32_t nc, int32_t nu_pre, int32_t nu_post, double omega,
+                     alefsi_mg* out);
+int alefsi_mg_destroy(alefsi_mg h);
+/* Enqueue on a caller-owned cudaStream_t (e.g. torch's current stream). */
+int alefsi_mg_set_stream(alefsi_mg h, void* stream);
+/* Capture the V-cycle once as a CUDA graph and replay it. */
+int alefsi_mg_use_graph(alefsi_mg h, int32_t on);
+
+/* Level operator MgLevel.matrix (reference linsolve.py:223; assembled by
+ * model.momentum_jacobian_data, model.py:297-381) in the split layout:
+ * nc x nc blocks on the Q2 cell-stencil pattern plus scalar
+ * pressure-pressure entries on the LPS macro pattern outside it.  A
+ * reference BlockPattern/data pair maps onto it exactly.
+ * HOST pointers; copied to HBM. */
+int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nnzb,
+                         const int64_t* indptr, const int32_t* indices, const double* data,
+                         int64_t nnz_pp, const int64_t* pp_indptr, const int32_t* pp_indices,
+                         const double* pp_data);
+
+/* PatchSet groups (reference mesh.py:446-480): n_groups homogeneous groups,
+ * patch_nodes concatenated group after group (node ids, patch-major).
+ * HOST pointers. */
+int alefsi_mg_set_patches(alefsi_mg h, int32_t level, int32_t n_groups,
+                          const int64_t* group_n_patches, const int32_t* group_nodes_per_patch,
+                          const int64_t* patch_nodes);
+
+/* MgLevel.P, scalar Q2 interpolation from level-1 to level as CSR over fine
+ * nodes (reference linsolve.py:183-216).  HOST pointers. */
+int alefsi_mg_set_prolongation(alefsi_mg h, int32_t level, int64_t n_fine, int64_t n_coarse,
+                               int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                               const double* vals);
+
+/* MgLevel.constrained, one byte per dof (reference linsolve.py:226). HOST. */
+int alefsi_mg_set_constrained(alefsi_mg h, int32_t level, const uint8_t* mask);
+
+/* VankaSmoother.factorize / patch_factorize on every level >= 1 and the
+ * coarse-level factorisation of MgSolver.__init__ (reference
+ * linsolve.py:120-134, 163-165, 236). */
+int alefsi_mg_factorize(alefsi_mg h);
+
+/* z = one V-cycle applied to b (MgSolver.dot, reference linsolve.py:238-255). */
+int alefsi_mg_apply(alefsi_mg h, const double* b, double* z, int32_t host_ptrs);
+
+/* y = A x (b == NULL) or y = b - A x on one level (DEVICE). */
+int alefsi_mg_spmv(alefsi_mg h, int32_t level, const double* x, const double* b, double* y);
+
+/* x <- one damped additive Vanka sweep (VankaSmoother.sweep,
+ * reference linsolve.py:167-178) (DEVICE). */
+int alefsi_mg_vanka_sweep(alefsi_mg h, int32_t level, double* x, const double* b);
+
+/* b_coarse = P^T r_fine with coarse constraints zeroed (MgSolver._restrict,
+ * reference linsolve.py:260-264) (DEVICE). */
+int alefsi_mg_restrict(alefsi_mg h, int32_t level, const double* r_fine, double* b_coarse);
+
+/* x_fine += P x_coarse with fine constraints zeroed (MgSolver._prolong +
+ * the update of linsolve.py:252, 266-270) (DEVICE). */
+int alefsi_mg_prolong_add(alefsi_mg h, int32_t level, const double* x_coarse, double* x_fine);
+
+/* x = A_0^{-1} b on the coarsest level (coarse_lu.solve, linsolve.py:246). */
+int alefsi_mg_coarse_solve(alefsi_mg h, const double* b, double* x);
+
+/* Copy the stored patch inverses of one group to host memory:
+ * (n_patches, np, ld) column-major with ld = np rounded up to even. */
+int alefsi_mg_get_inverses(alefsi_mg h, int32_t level, int32_t group, double* out);
+
+/* info[0..7] = n_nodes, ndof, nnzb, nnz_pp, n_groups, Y size, inverse doubles, ld. */
+int alefsi_mg_info(alefsi_mg h, int32_t level, int64_t* info);
+
+/* Right-preconditioned, unrestarted GMRES with the V-cycle as
+ * preconditioner (gmres, reference linsolve.py:41-115): classical
+ * Gram-Schmidt with the conditional second pass, Givens rotations,
+ * residuals[0..iterations] = the reference's stats.residuals.  Returns
+ * ALEFSI_ERR_NOT_CONVERGED (x and residuals still written) when max_iter is
+ * reached above tolerance. */
+int alefsi_gmres(alefsi_mg h, const double* b, double* x, double rel_tol, double abs_tol,
+                 int32_t max_iter, int32_t host_ptrs, double* residuals, int32_t* iterations,
+                 int32_t* converged);
+/* Pre-allocate the Krylov basis for max_iter iterations. */
+int alefsi_gmres_workspace(alefsi_mg h, int32_t max_iter);
+/* Number of device kernels this handle has enqueued (graph replays excluded). */
+int alefsi_kernel_stats(alefsi_mg h, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ALEFSI_B200_H */

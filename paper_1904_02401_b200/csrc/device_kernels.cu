@@ -1,0 +1,692 @@
+// Device kernels of the MG-GMRES / Vanka linear-solve path, sm_100a, FP64.
+//
+// Every kernel here is HBM- (or L2-) bandwidth bound: the operator is a
+// block-sparse FEM stencil and the smoother is a batch of distinct small
+// dense inverses, so there is no GEMM-shaped work for the tensor cores.
+// Design rules followed throughout: coalesced 16-byte streaming loads with
+// evict-first hints for data read once per sweep (operator blocks, patch
+// inverses), read-only-path loads for vectors reused from L2, and fixed-order
+// reductions so that every result is bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_kernels.cuh"
+
+namespace alefsi {
+
+namespace {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-shape block reduction (blockDim.x == 256): deterministic.
+__device__ __forceinline__ double block_sum_256(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = l < 8 ? red[l] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;  // valid in thread 0
+}
+
+inline int grid_for(int64_t n, int per_block) { return (int)((n + per_block - 1) / per_block); }
+
+// --------------------------------------------------------------------------
+// Block-sparse matrix-vector product.  One warp per block row (mesh node).
+// NC = 4: lane = 4*blk + r, each lane streams one 32-byte block row
+// (2 x 16-byte loads), 8 blocks = 1 KiB per warp iteration; rows are summed
+// with xor-shuffles over lanes sharing r.  NC = 3: lane = 3*blk + r over 30
+// lanes, 8-byte loads (blocks are 72 bytes), per-r butterfly reductions.
+// The scalar pressure extension L is swept by the same warp afterwards.
+// --------------------------------------------------------------------------
+template <int NC, int MODE>
+__global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __restrict__ indptr,
+                                                   const int32_t* __restrict__ indices,
+                                                   const double* __restrict__ data,
+                                                   const int64_t* __restrict__ pp_ptr,
+                                                   const int32_t* __restrict__ pp_idx,
+                                                   const double* __restrict__ pp_val,
+                                                   const double* __restrict__ x,
+                                                   const double* __restrict__ b,
+                                                   double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  constexpr int BPI = kWarp / NC;  // blocks per warp iteration
+  const int r = lane % NC;
+  const int sub = lane / NC;
+  const int64_t beg = indptr[row], end = indptr[row + 1];
+  double acc = 0.0;
+  if (sub < BPI) {
+    for (int64_t blk = beg + sub; blk < end; blk += BPI) {
+      const int64_t col = __ldcs(indices + blk);
+      const double* v = data + blk * (NC * NC) + r * NC;
+      const double* xv = x + col * NC;
+      if constexpr (NC == 4) {
+        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(v));
+        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(v) + 1);
+        const double2 x0 = __ldg(reinterpret_cast<const double2*>(xv));
+        const double2 x1 = __ldg(reinterpret_cast<const double2*>(xv) + 1);
+        acc = fma(v0.x, x0.x, acc);
+        acc = fma(v0.y, x0.y, acc);
+        acc = fma(v1.x, x1.x, acc);
+        acc = fma(v1.y, x1.y, acc);
+      } else {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc = fma(__ldcs(v + c), __ldg(xv + c), acc);
+      }
+    }
+  }
+  // pressure extension: sum_e L[row, e] * x[col_e, 0]
+  double accp = 0.0;
+  if (pp_ptr != nullptr) {
+    const int64_t pb = pp_ptr[row], pe = pp_ptr[row + 1];
+    for (int64_t e = pb + lane; e < pe; e += kWarp)
+      accp = fma(__ldcs(pp_val + e), __ldg(x + (int64_t)__ldcs(pp_idx + e) * NC), accp);
+    accp = warp_sum(accp);
+  }
+  double out[NC];
+  if constexpr (NC == 4) {
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+    // lanes 0..3 now hold rows 0..3
+    if (lane < NC) {
+      double v = acc + (lane == 0 ? accp : 0.0);
+      const int64_t o = row * NC + lane;
+      y[o] = MODE == 1 ? b[o] - v : v;
+    }
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < NC; ++rr) out[rr] = warp_sum((r == rr && sub < BPI) ? acc : 0.0);
+    if (lane < NC) {
+      double v = out[0];
+#pragma unroll
+      for (int rr = 1; rr < NC; ++rr)
+        if (lane == rr) v = out[rr];
+      if (lane == 0) v += accp;
+      const int64_t o = row * NC + lane;
+      y[o] = MODE == 1 ? b[o] - v : v;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Vanka apply: Y[p] = A_p^{-1} d[dofs_p].  Inverses are stored column-major
+// with an even column length LD, so thread t of a patch owns rows 2t, 2t+1
+// and streams one 16-byte pair per column: a patch column is one contiguous
+// LD*8-byte run, read exactly once per sweep with evict-first loads.  The
+// patch defect is staged in shared memory and broadcast.
+// --------------------------------------------------------------------------
+template <int NP, int LD, int NC>
+__global__ void __launch_bounds__(128) vanka_apply_kernel(int64_t n_patches,
+                                                          const int32_t* __restrict__ nodes,
+                                                          const double* __restrict__ inv,
+                                                          const double* __restrict__ d,
+                                                          double* __restrict__ Y) {
+  constexpr int NPN = NP / NC;
+  constexpr int TPP = ((LD / 2 + 31) / 32) * 32;  // threads per patch
+  constexpr int PPC = 128 / TPP;                  // patches per CTA
+  static_assert(PPC >= 1, "patch too large for one CTA");
+  __shared__ double ds[PPC][LD];
+  const int sub = threadIdx.x / TPP, t = threadIdx.x % TPP;
+  const int64_t p = (int64_t)blockIdx.x * PPC + sub;
+  const bool valid = p < n_patches;
+  if (valid) {
+    for (int j = t; j < NP; j += TPP) {
+      const int a = j / NC, c = j - a * NC;
+      ds[sub][j] = __ldg(d + (int64_t)__ldg(nodes + p * NPN + a) * NC + c);
+    }
+  }
+  __syncthreads();
+  if (!valid || 2 * t >= LD) return;
+  const double2* col = reinterpret_cast<const double2*>(inv + p * (int64_t)(NP * LD)) + t;
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 12
+  for (int j = 0; j < NP; ++j) {
+    const double2 v = __ldcs(col + j * (LD / 2));
+    const double dj = ds[sub][j];
+    acc.x = fma(v.x, dj, acc.x);
+    acc.y = fma(v.y, dj, acc.y);
+  }
+  reinterpret_cast<double2*>(Y + p * (int64_t)LD)[t] = acc;
+}
+
+// Deterministic scatter-add of the weighted patch corrections: each dof sums
+// its patches' rows in ascending patch order (the reference's np.add.at
+// order, linsolve.py:171-178) and applies x + omega * upd.
+__global__ void vanka_gather_kernel(int64_t ndof, int nc, const int64_t* __restrict__ gptr,
+                                    const int64_t* __restrict__ goff,
+                                    const double* __restrict__ w, const double* __restrict__ Y,
+                                    double* __restrict__ x, double omega, int init_zero) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ndof) return;
+  const int64_t n = t / nc;
+  const int c = (int)(t - n * nc);
+  const double wn = __ldg(w + n);
+  double acc = 0.0;
+  for (int64_t s = gptr[n]; s < gptr[n + 1]; ++s)
+    acc = __dadd_rn(acc, __dmul_rn(wn, __ldg(Y + goff[s] + c)));
+  const double base = init_zero ? 0.0 : x[t];
+  x[t] = __dadd_rn(base, __dmul_rn(omega, acc));
+}
+
+// Gather A_p = R_p A R_p^T into shared memory and invert it in place by
+// Gauss-Jordan elimination with partial (row) pivoting; columns are
+// unscrambled at the end.  One CTA per patch.
+template <int NP, int NC>
+__global__ void __launch_bounds__(256) vanka_factorize_kernel(DevMatrix A, int64_t n_patches,
+                                                              const int32_t* __restrict__ nodes,
+                                                              double* __restrict__ inv, int ld,
+                                                              int64_t* status) {
+  constexpr int NPN = NP / NC;
+  extern __shared__ double smem[];
+  double* M = smem;                                   // NP*NP row-major
+  double* colk = M + NP * NP;                         // NP
+  int64_t* slotB = reinterpret_cast<int64_t*>(colk + NP);
+  int64_t* slotP = slotB + NPN * NPN;
+  int* perm = reinterpret_cast<int*>(slotP + NPN * NPN);
+  __shared__ int piv_row;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int64_t p = blockIdx.x;
+  if (p >= n_patches) return;
+  const int32_t* pn = nodes + p * NPN;
+  for (int t = tid; t < NPN * NPN; t += bd) {
+    const int a = t / NPN, b = t - a * NPN;
+    const int64_t ra = pn[a];
+    const int32_t cb = pn[b];
+    int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
+    }
+    slotB[t] = (lo < A.indptr[ra + 1] && A.indices[lo] == cb) ? lo : -1;
+    int64_t sp = -1;
+    if (slotB[t] < 0 && A.pp_indptr != nullptr) {
+      lo = A.pp_indptr[ra];
+      hi = A.pp_indptr[ra + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
+      }
+      if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) sp = lo;
+    }
+    slotP[t] = sp;
+  }
+  __syncthreads();
+  for (int e = tid; e < NP * NP; e += bd) {
+    const int i = e / NP, j = e - i * NP;
+    const int a = i / NC, ci = i - a * NC, b = j / NC, cj = j - b * NC;
+    const int t = a * NPN + b;
+    double v = 0.0;
+    if (slotB[t] >= 0) v = A.data[slotB[t] * (NC * NC) + ci * NC + cj];
+    else if (ci == 0 && cj == 0 && slotP[t] >= 0) v = A.pp_data[slotP[t]];
+    M[e] = v;
+  }
+  __syncthreads();
+  for (int k = 0; k < NP; ++k) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < NP; i += 32) {
+        const double v = fabs(M[i * NP + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) { piv_row = bi; perm[k] = bi; }
+    }
+    __syncthreads();
+    const int pr = piv_row;
+    if (pr != k)
+      for (int j = tid; j < NP; j += bd) {
+        const double tmp = M[k * NP + j];
+        M[k * NP + j] = M[pr * NP + j];
+        M[pr * NP + j] = tmp;
+      }
+    __syncthreads();
+    const double piv = M[k * NP + k];
+    if (piv == 0.0) {
+      if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
+                              (unsigned long long)(p + 1));
+      return;
+    }
+    const double rp = 1.0 / piv;
+    for (int i = tid; i < NP; i += bd) colk[i] = M[i * NP + k];
+    __syncthreads();
+    for (int j = tid; j < NP; j += bd) M[k * NP + j] = (j == k) ? rp : M[k * NP + j] * rp;
+    __syncthreads();
+    for (int e = tid; e < NP * NP; e += bd) {
+      const int i = e / NP, j = e - i * NP;
+      if (i == k) continue;
+      const double f = colk[i];
+      M[e] = (j == k) ? -f * rp : M[e] - f * M[k * NP + j];
+    }
+    __syncthreads();
+  }
+  for (int k = NP - 1; k >= 0; --k) {
+    const int pr = perm[k];
+    if (pr != k)
+      for (int i = tid; i < NP; i += bd) {
+        const double tmp = M[i * NP + k];
+        M[i * NP + k] = M[i * NP + pr];
+        M[i * NP + pr] = tmp;
+      }
+    __syncthreads();
+  }
+  double* out = inv + p * (int64_t)NP * ld;
+  for (int e = tid; e < NP * ld; e += bd) {
+    const int j = e / ld, i = e - j * ld;
+    out[e] = i < NP ? M[i * NP + j] : 0.0;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Grid transfer: Q2 interpolation P (fine rows) and its transpose (coarse
+// rows), applied per component with the constrained-dof masks of
+// linsolve.py:260-270.  Summation order follows the stored column order
+// (fine-node order for the transpose, as in scipy's CSC matvec).
+// --------------------------------------------------------------------------
+__global__ void transfer_kernel(int64_t nrows, int nc, const int64_t* __restrict__ ptr,
+                                const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                const double* __restrict__ src,
+                                const uint8_t* __restrict__ constrained,
+                                double* __restrict__ dst, int add) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nrows * nc) return;
+  const int64_t row = t / nc;
+  const int c = (int)(t - row * nc);
+  double acc = 0.0;
+  for (int64_t e = ptr[row]; e < ptr[row + 1]; ++e)
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(val + e), __ldg(src + (int64_t)__ldg(idx + e) * nc + c)));
+  if (constrained[t]) acc = 0.0;
+  dst[t] = add ? __dadd_rn(dst[t], acc) : acc;
+}
+
+// --------------------------------------------------------------------------
+// Coarse level: dense Gauss-Jordan inverse (one pivot step per launch pair)
+// and a warp-per-row dense matvec.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) gj_pivot_kernel(double* M, int64_t n, int64_t k,
+                                                        int64_t* perm, double* colk,
+                                                        double* rp_out, int64_t* status) {
+  __shared__ double sb[32];
+  __shared__ int64_t si[32];
+  __shared__ int64_t prow;
+  const int tid = threadIdx.x;
+  double best = -1.0;
+  int64_t bi = k;
+  for (int64_t i = k + tid; i < n; i += blockDim.x) {
+    const double v = fabs(M[i * n + k]);
+    if (v > best) { best = v; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if ((tid & 31) == 0) { sb[tid >> 5] = best; si[tid >> 5] = bi; }
+  __syncthreads();
+  if (tid < 32) {
+    best = tid < (int)(blockDim.x >> 5) ? sb[tid] : -2.0;
+    bi = tid < (int)(blockDim.x >> 5) ? si[tid] : n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (tid == 0) { prow = bi; perm[k] = bi; }
+  }
+  __syncthreads();
+  const int64_t pr = prow;
+  if (pr != k)
+    for (int64_t j = tid; j < n; j += blockDim.x) {
+      const double t = M[k * n + j];
+      M[k * n + j] = M[pr * n + j];
+      M[pr * n + j] = t;
+    }
+  __syncthreads();
+  const double piv = M[k * n + k];
+  if (piv == 0.0) {
+    if (tid == 0 && *status == 0) *status = k + 1;
+    if (tid == 0) *rp_out = 0.0;
+    return;
+  }
+  const double rp = 1.0 / piv;
+  for (int64_t i = tid; i < n; i += blockDim.x) colk[i] = M[i * n + k];
+  __syncthreads();
+  for (int64_t j = tid; j < n; j += blockDim.x) M[k * n + j] = (j == k) ? rp : M[k * n + j] * rp;
+  if (tid == 0) *rp_out = rp;
+}
+
+__global__ void gj_eliminate_kernel(double* M, int64_t n, int64_t k, const double* colk,
+                                    const double* rp_in) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const int64_t i = e / n, j = e - i * n;
+  if (i == k) return;
+  const double rp = *rp_in;
+  if (rp == 0.0) return;
+  const double f = colk[i];
+  M[e] = (j == k) ? -f * rp : M[e] - f * M[k * n + j];
+}
+
+__global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double* row = M + i * n;
+  for (int64_t k = n - 1; k >= 0; --k) {
+    const int64_t p = perm[k];
+    if (p != k) {
+      const double t = row[k];
+      row[k] = row[p];
+      row[p] = t;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) dense_matvec_kernel(int64_t n, const double* __restrict__ M,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  const double* r = M + row * n;
+  double acc = 0.0;
+  for (int64_t j = lane; j < n; j += 32) acc = fma(__ldg(r + j), __ldg(x + j), acc);
+  acc = warp_sum(acc);
+  if (lane == 0) y[row] = acc;
+}
+
+// --------------------------------------------------------------------------
+// Krylov vector kernels.  Two-stage fixed-order reductions: kRedBlocks
+// partial sums per output, then one CTA per output sums its partials.
+// --------------------------------------------------------------------------
+constexpr int kBatch = 8;
+
+__global__ void __launch_bounds__(256) multi_dot_kernel(int nvec, const double* __restrict__ V,
+                                                        int64_t ldv, const double* __restrict__ w,
+                                                        int64_t n, double* __restrict__ partial,
+                                                        const int* flag) {
+  if (flag != nullptr && *flag == 0) return;
+  __shared__ double red[8];
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+  const int nout = nvec + 1;
+  for (int j0 = 0; j0 < nvec; j0 += kBatch) {
+    double acc[kBatch];
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) acc[q] = 0.0;
+    for (int64_t i = gt; i < n; i += gs) {
+      const double wi = __ldg(w + i);
+#pragma unroll
+      for (int q = 0; q < kBatch; ++q)
+        if (j0 + q < nvec) acc[q] = fma(__ldg(V + (int64_t)(j0 + q) * ldv + i), wi, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < kBatch; ++q) {
+      if (j0 + q >= nvec) break;
+      const double s = block_sum_256(acc[q], red);
+      if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * nout + j0 + q] = s;
+    }
+  }
+  double sq = 0.0;
+  for (int64_t i = gt; i < n; i += gs) {
+    const double wi = __ldg(w + i);
+    sq = fma(wi, wi, sq);
+  }
+  const double s = block_sum_256(sq, red);
+  if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * nout + nvec] = s;
+}
+
+__global__ void __launch_bounds__(256) reduce_partials_kernel(int nout, int nblocks,
+                                                              const double* __restrict__ partial,
+                                                              double* __restrict__ out,
+                                                              const int* flag) {
+  if (flag != nullptr && *flag == 0) return;
+  __shared__ double red[8];
+  const int j = blockIdx.x;
+  double acc = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partial[(int64_t)b * nout + j];
+  const double s = block_sum_256(acc, red);
+  if (threadIdx.x == 0) out[j] = s;
+}
+
+__global__ void __launch_bounds__(256) multi_axpy_kernel(int nvec, const double* __restrict__ V,
+                                                         int64_t ldv, const double* __restrict__ h,
+                                                         double* __restrict__ w, int64_t n,
+                                                         double* __restrict__ partial,
+                                                         const int* flag) {
+  if (flag != nullptr && *flag == 0) return;
+  __shared__ double hs[512];
+  __shared__ double red[8];
+  for (int j = threadIdx.x; j < nvec; j += blockDim.x) hs[j] = h[j];
+  __syncthreads();
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+  double sq = 0.0;
+  for (int64_t i = gt; i < n; i += gs) {
+    double acc = 0.0;
+    for (int j = 0; j < nvec; ++j) acc = fma(hs[j], __ldg(V + (int64_t)j * ldv + i), acc);
+    const double wi = w[i] - acc;
+    w[i] = wi;
+    sq = fma(wi, wi, sq);
+  }
+  const double s = block_sum_256(sq, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// stage 0: decide re-orthogonalisation (Kahan test of linsolve.py:79-83);
+// stage 1: fold the second projection into the Hessenberg column and set
+// H[k+1, k] = ||w||.
+__global__ void arnoldi_finish_kernel(int k, double* hcol, const double* h2, const double* nb2,
+                                      const double* na2, int* flag, int stage) {
+  if (stage == 0) {
+    if (threadIdx.x == 0) *flag = (sqrt(*na2) < 0.7071 * sqrt(*nb2)) ? 1 : 0;
+    return;
+  }
+  if (*flag)
+    for (int j = threadIdx.x; j <= k; j += blockDim.x) hcol[j] += h2[j];
+  if (threadIdx.x == 0) hcol[k + 1] = sqrt(*na2);
+}
+
+__global__ void scale_copy_kernel(const double* __restrict__ w, double* __restrict__ v,
+                                  const double* hkk1, int64_t n) {
+  const double h = *hkk1;
+  if (!(h > 0.0)) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = w[i] / h;
+}
+
+__global__ void div_kernel(const double* __restrict__ x, double* __restrict__ y, double a,
+                           int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i] / a;
+}
+
+__global__ void combine_kernel(int nvec, const double* __restrict__ V, int64_t ldv,
+                               const double* __restrict__ c, double* __restrict__ y, int64_t n) {
+  __shared__ double cs[512];
+  for (int j = threadIdx.x; j < nvec; j += blockDim.x) cs[j] = c[j];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < nvec; ++j) acc = fma(cs[j], __ldg(V + (int64_t)j * ldv + i), acc);
+    y[i] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x, int64_t n,
+                                                    double* __restrict__ partial) {
+  __shared__ double red[8];
+  double sq = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    sq = fma(x[i], x[i], sq);
+  const double s = block_sum_256(sq, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+template <int NC>
+void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
+                   cudaStream_t s) {
+  const int grid = grid_for(A.n_nodes * 32, 256);
+  if (mode == 0)
+    spmv_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
+                                            A.pp_indices, A.pp_data, x, b, y);
+  else
+    spmv_kernel<NC, 1><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
+                                            A.pp_indices, A.pp_data, x, b, y);
+}
+
+template <int NP, int LD, int NC>
+void apply_dispatch(const DevPatchGroup& g, const double* d, double* Y, cudaStream_t s) {
+  constexpr int TPP = ((LD / 2 + 31) / 32) * 32;
+  constexpr int PPC = 128 / TPP;
+  const int grid = grid_for(g.n_patches, PPC);
+  vanka_apply_kernel<NP, LD, NC><<<grid, 128, 0, s>>>(g.n_patches, g.nodes, g.inv, d,
+                                                       Y + g.y_offset);
+}
+
+template <int NP, int NC>
+void factorize_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
+                        cudaStream_t s) {
+  constexpr int NPN = NP / NC;
+  const size_t smem = sizeof(double) * (NP * NP + NP) + sizeof(int64_t) * 2 * NPN * NPN +
+                      sizeof(int) * NP;
+  cudaFuncSetAttribute(vanka_factorize_kernel<NP, NC>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  vanka_factorize_kernel<NP, NC><<<(unsigned)g.n_patches, 256, smem, s>>>(A, g.n_patches, g.nodes,
+                                                                         g.inv, g.ld, status);
+}
+
+}  // namespace
+
+void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
+                 cudaStream_t s) {
+  if (A.n_nodes == 0) return;
+  if (A.nc == 4) spmv_dispatch<4>(A, x, b, y, mode, s);
+  else if (A.nc == 3) spmv_dispatch<3>(A, x, b, y, mode, s);
+}
+
+void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
+                            cudaStream_t s) {
+  if (g.n_patches == 0) return;
+  if (A.nc == 3 && g.np == 27) factorize_dispatch<27, 3>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 75) factorize_dispatch<75, 3>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108) factorize_dispatch<108, 4>(A, g, status, s);
+  else if (A.nc == 2 && g.np == 18) factorize_dispatch<18, 2>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 81) factorize_dispatch<81, 3>(A, g, status, s);
+}
+
+void launch_vanka_apply(const DevPatchGroup& g, int nc, const double* d, double* Y,
+                        cudaStream_t s) {
+  if (g.n_patches == 0) return;
+  if (nc == 3 && g.np == 27) apply_dispatch<27, 28, 3>(g, d, Y, s);
+  else if (nc == 3 && g.np == 75) apply_dispatch<75, 76, 3>(g, d, Y, s);
+  else if (nc == 4 && g.np == 108) apply_dispatch<108, 108, 4>(g, d, Y, s);
+  else if (nc == 2 && g.np == 18) apply_dispatch<18, 18, 2>(g, d, Y, s);
+  else if (nc == 3 && g.np == 81) apply_dispatch<81, 82, 3>(g, d, Y, s);
+}
+
+void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int64_t* goff,
+                         const double* weight, const double* Y, double* x, double omega,
+                         int init_zero, cudaStream_t s) {
+  const int64_t ndof = n_nodes * nc;
+  if (ndof == 0) return;
+  vanka_gather_kernel<<<grid_for(ndof, 256), 256, 0, s>>>(ndof, nc, gptr, goff, weight, Y, x,
+                                                           omega, init_zero);
+}
+
+void launch_restrict(int64_t n_coarse, int nc, const int64_t* ptr, const int32_t* idx,
+                     const double* val, const double* r_fine, const uint8_t* constrained_coarse,
+                     double* b_coarse, cudaStream_t s) {
+  transfer_kernel<<<grid_for(n_coarse * nc, 256), 256, 0, s>>>(
+      n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
+}
+
+void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_t* idx,
+                        const double* val, const double* x_coarse,
+                        const uint8_t* constrained_fine, double* x_fine, cudaStream_t s) {
+  transfer_kernel<<<grid_for(n_fine * nc, 256), 256, 0, s>>>(
+      n_fine, nc, ptr, idx, val, x_coarse, constrained_fine, x_fine, 1);
+}
+
+int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s) {
+  // work: colk (n doubles) | rp (1 double) | perm (n int64)
+  double* colk = work;
+  double* rp = work + n;
+  int64_t* perm = reinterpret_cast<int64_t*>(work + n + 1);
+  cudaMemsetAsync(status, 0, sizeof(int64_t), s);
+  const int grid = grid_for(n * n, 256);
+  for (int64_t k = 0; k < n; ++k) {
+    gj_pivot_kernel<<<1, 1024, 0, s>>>(M, n, k, perm, colk, rp, status);
+    gj_eliminate_kernel<<<grid, 256, 0, s>>>(M, n, k, colk, rp);
+  }
+  gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm);
+  return 0;
+}
+
+void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
+                         cudaStream_t s) {
+  dense_matvec_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, M, x, y);
+}
+
+void launch_multi_dot(int nvec, const double* V, int64_t ldv, const double* w, int64_t n,
+                      double* partial, double* out, const int* flag, cudaStream_t s) {
+  multi_dot_kernel<<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, w, n, partial, flag);
+  reduce_partials_kernel<<<nvec + 1, 256, 0, s>>>(nvec + 1, kRedBlocks, partial, out, flag);
+}
+
+void launch_multi_axpy(int nvec, const double* V, int64_t ldv, const double* h, double* w,
+                       int64_t n, double* partial, double* out, const int* flag,
+                       cudaStream_t s) {
+  multi_axpy_kernel<<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, h, w, n, partial, flag);
+  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, out, flag);
+}
+
+void launch_arnoldi_finish(int k, double* hcol, double* h2, const double* nb2, double* na2,
+                           int* flag, int stage, cudaStream_t s) {
+  arnoldi_finish_kernel<<<1, 256, 0, s>>>(k, hcol, h2, nb2, na2, flag, stage);
+}
+
+void launch_scale_copy(const double* w, double* v, const double* hkk1, int64_t n,
+                       cudaStream_t s) {
+  scale_copy_kernel<<<kRedBlocks, 256, 0, s>>>(w, v, hkk1, n);
+}
+
+void launch_scale(const double* x, double* y, double alpha, int64_t n, cudaStream_t s) {
+  div_kernel<<<kRedBlocks, 256, 0, s>>>(x, y, alpha, n);
+}
+
+void launch_combine(int nvec, const double* V, int64_t ldv, const double* c, double* y,
+                    int64_t n, cudaStream_t s) {
+  combine_kernel<<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, c, y, n);
+}
+
+void launch_sumsq(const double* x, int64_t n, double* partial, double* out, cudaStream_t s) {
+  sumsq_kernel<<<kRedBlocks, 256, 0, s>>>(x, n, partial);
+  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, out, nullptr);
+}
+
+}  // namespace alefsi

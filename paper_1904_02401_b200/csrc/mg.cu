@@ -1,0 +1,816 @@
+// Device-resident multigrid hierarchy, V-cycle and right-preconditioned
+// GMRES behind the C ABI of include/alefsi_b200.h.
+//
+// Mirrors the reference solver objects (reference pkg/src/alefsi/linsolve.py):
+//   gmres                 linsolve.py:41-115   -> alefsi_gmres
+//   patch_factorize       linsolve.py:120-134  -> alefsi_mg_factorize
+//   VankaSmoother.sweep   linsolve.py:167-178  -> alefsi_mg_vanka_sweep
+//   MgSolver._cycle       linsolve.py:243-255  -> alefsi_mg_apply
+//   MgSolver._restrict    linsolve.py:260-264  -> alefsi_mg_restrict
+//   MgSolver._prolong     linsolve.py:266-270  -> alefsi_mg_prolong_add
+//   coarse_lu.solve       linsolve.py:236,246  -> alefsi_mg_coarse_solve
+// The per-level operators, patch inverses, transfer operators and Krylov
+// basis live in HBM for the lifetime of the handle; the host only runs the
+// Givens rotations of the (max_iter+1) x max_iter Hessenberg matrix.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "alefsi_common.h"
+#include "alefsi_b200.h"
+#include "device_kernels.cuh"
+
+namespace alefsi {
+namespace {
+
+#define CK(expr)                                                                  \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess)                                                        \
+      return fail(ALEFSI_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      reset();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t alloc(size_t count) {
+    reset();
+    n = count;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc(&p, count * sizeof(T));
+  }
+  cudaError_t upload(const T* host, size_t count, cudaStream_t s) {
+    cudaError_t e = alloc(count);
+    if (e != cudaSuccess || count == 0) return e;
+    return cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s);
+  }
+};
+
+struct Group {
+  int npn = 0, np = 0, ld = 0;
+  int64_t n_patches = 0, y_offset = 0;
+  DevBuf<int32_t> nodes;
+  DevBuf<double> inv;
+};
+
+struct Level {
+  int64_t n_nodes = 0;
+  int nc = 0;
+  bool has_matrix = false;
+  int64_t nnzb = 0, nnz_pp = 0;
+  DevBuf<int64_t> indptr, pp_indptr;
+  DevBuf<int32_t> indices, pp_indices;
+  DevBuf<double> data, pp_data;
+  std::vector<double> host_dense;   // level 0 only: dense copy for the coarse inverse
+  std::vector<std::unique_ptr<Group>> groups;
+  DevBuf<double> Y;
+  DevBuf<int64_t> gptr, goff;
+  DevBuf<double> weight;
+  bool has_P = false;
+  int64_t n_coarse = 0;
+  DevBuf<int64_t> P_ptr, R_ptr;
+  DevBuf<int32_t> P_idx, R_idx;
+  DevBuf<double> P_val, R_val;
+  DevBuf<uint8_t> constrained;
+  DevBuf<double> x, b, d;
+
+  int64_t ndof() const { return n_nodes * nc; }
+  DevMatrix mat() const {
+    DevMatrix m;
+    m.nc = nc;
+    m.n_nodes = n_nodes;
+    m.nnzb = nnzb;
+    m.nnz_pp = nnz_pp;
+    m.indptr = indptr.p;
+    m.indices = indices.p;
+    m.data = data.p;
+    m.pp_indptr = nnz_pp > 0 ? pp_indptr.p : nullptr;
+    m.pp_indices = pp_indices.p;
+    m.pp_data = pp_data.p;
+    return m;
+  }
+};
+
+}  // namespace
+
+struct MgHandle {
+  int n_levels = 0, nc = 0, nu_pre = 2, nu_post = 2;
+  double omega = 0.8;
+  std::vector<Level> lv;
+  DevBuf<double> coarse_inv, coarse_work;
+  DevBuf<int64_t> status;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool factorized = false;
+  // graph-captured V-cycle (fixed in/out buffers)
+  bool use_graph = false;
+  bool graph_valid = false;
+  cudaGraphExec_t graph_exec = nullptr;
+  DevBuf<double> g_in, g_out;
+  // GMRES workspace
+  int v_cap = 0;
+  DevBuf<double> V, w, z, t, xb, bb, partial, tmp, tmp2, scal;
+  DevBuf<int> flag;
+  double* pinned = nullptr;
+  int64_t kernel_launches = 0;
+
+  ~MgHandle() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (pinned) cudaFreeHost(pinned);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  Level& fine() { return lv.back(); }
+
+  // ---------------------------------------------------------------- V-cycle
+  void sweep(Level& L, const double* b, double* x, bool zero) {
+    const double* d = b;
+    if (!zero) {
+      launch_spmv(L.mat(), x, b, L.d.p, 1, stream);
+      ++kernel_launches;
+      d = L.d.p;
+    }
+    for (auto& g : L.groups) {
+      DevPatchGroup dg;
+      dg.npn = g->npn;
+      dg.np = g->np;
+      dg.ld = g->ld;
+      dg.n_patches = g->n_patches;
+      dg.nodes = g->nodes.p;
+      dg.inv = g->inv.p;
+      dg.y_offset = g->y_offset;
+      launch_vanka_apply(dg, L.nc, d, L.Y.p, stream);
+      ++kernel_launches;
+    }
+    launch_vanka_gather(L.n_nodes, L.nc, L.gptr.p, L.goff.p, L.weight.p, L.Y.p, x, omega,
+                        zero ? 1 : 0, stream);
+    ++kernel_launches;
+  }
+
+  void cycle(int l, const double* b, double* x) {
+    Level& L = lv[l];
+    if (l == 0) {
+      launch_dense_matvec(L.ndof(), coarse_inv.p, b, x, stream);
+      ++kernel_launches;
+      return;
+    }
+    bool zero = true;
+    for (int s = 0; s < nu_pre; ++s) {
+      sweep(L, b, x, zero);
+      zero = false;
+    }
+    if (zero) cudaMemsetAsync(x, 0, sizeof(double) * L.ndof(), stream);
+    launch_spmv(L.mat(), x, b, L.d.p, 1, stream);
+    Level& C = lv[l - 1];
+    launch_restrict(C.n_nodes, C.nc, L.R_ptr.p, L.R_idx.p, L.R_val.p, L.d.p, C.constrained.p,
+                    C.b.p, stream);
+    kernel_launches += 2;
+    cycle(l - 1, C.b.p, C.x.p);
+    launch_prolong_add(L.n_nodes, L.nc, L.P_ptr.p, L.P_idx.p, L.P_val.p, C.x.p,
+                       L.constrained.p, x, stream);
+    ++kernel_launches;
+    for (int s = 0; s < nu_post; ++s) sweep(L, b, x, false);
+  }
+
+  int apply(const double* b, double* x) {
+    if (!factorized) return fail(ALEFSI_ERR_STATE, "mg_apply before mg_factorize");
+    const int64_t n = fine().ndof();
+    if (!use_graph) {
+      cycle(n_levels - 1, b, x);
+      CK(cudaGetLastError());
+      return ALEFSI_OK;
+    }
+    if (!graph_valid) {
+      CK(g_in.alloc(n));
+      CK(g_out.alloc(n));
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      cycle(n_levels - 1, g_in.p, g_out.p);
+      CK(cudaStreamEndCapture(stream, &graph));
+      CK(cudaGraphInstantiate(&graph_exec, graph, 0));
+      cudaGraphDestroy(graph);
+      graph_valid = true;
+    }
+    CK(cudaMemcpyAsync(g_in.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+    CK(cudaGraphLaunch(graph_exec, stream));
+    CK(cudaMemcpyAsync(x, g_out.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+    return ALEFSI_OK;
+  }
+
+  // ------------------------------------------------------------ factorize
+  int factorize() {
+    for (int l = 1; l < n_levels; ++l) {
+      Level& L = lv[l];
+      if (!L.has_matrix) return fail(ALEFSI_ERR_STATE, "level matrix missing");
+      if (!L.has_P) return fail(ALEFSI_ERR_STATE, "level prolongation missing");
+      if (L.groups.empty()) return fail(ALEFSI_ERR_STATE, "level patches missing");
+      if (!L.constrained.p || !lv[l - 1].constrained.p)
+        return fail(ALEFSI_ERR_STATE, "constrained mask missing");
+      CK(cudaMemsetAsync(status.p, 0, sizeof(int64_t), stream));
+      int64_t off = 0;
+      for (auto& g : L.groups) {
+        CK(g->inv.alloc((size_t)g->n_patches * g->np * g->ld));
+        DevPatchGroup dg;
+        dg.npn = g->npn;
+        dg.np = g->np;
+        dg.ld = g->ld;
+        dg.n_patches = g->n_patches;
+        dg.nodes = g->nodes.p;
+        dg.inv = g->inv.p;
+        launch_vanka_factorize(L.mat(), dg, status.p, stream);
+        CK(cudaGetLastError());
+        int64_t st = 0;
+        CK(cudaMemcpyAsync(&st, status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (st != 0)
+          return fail(ALEFSI_ERR_SINGULAR,
+                      "singular Vanka patch block: level " + std::to_string(l) + " patch " +
+                          std::to_string(off + st - 1));
+        off += g->n_patches;
+      }
+    }
+    // coarse level: dense inverse
+    Level& C = lv[0];
+    if (!C.has_matrix) return fail(ALEFSI_ERR_STATE, "coarse matrix missing");
+    const int64_t n0 = C.ndof();
+    CK(coarse_inv.upload(C.host_dense.data(), (size_t)n0 * n0, stream));
+    CK(coarse_work.alloc(2 * n0 + 2));
+    dense_inverse(coarse_inv.p, n0, coarse_work.p, status.p, stream);
+    CK(cudaGetLastError());
+    int64_t st = 0;
+    CK(cudaMemcpyAsync(&st, status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (st != 0) return fail(ALEFSI_ERR_SINGULAR, "singular coarse-level matrix");
+    for (int l = 0; l < n_levels; ++l) {
+      Level& L = lv[l];
+      CK(L.x.alloc(L.ndof()));
+      CK(L.b.alloc(L.ndof()));
+      CK(L.d.alloc(L.ndof()));
+    }
+    factorized = true;
+    graph_valid = false;
+    return ALEFSI_OK;
+  }
+
+  // ----------------------------------------------------------------- GMRES
+  int ensure_workspace(int max_iter) {
+    const int64_t n = fine().ndof();
+    if (v_cap < max_iter + 1) {
+      CK(V.alloc((size_t)(max_iter + 1) * n));
+      v_cap = max_iter + 1;
+    }
+    if (w.n != (size_t)n) {
+      CK(w.alloc(n));
+      CK(z.alloc(n));
+      CK(t.alloc(n));
+      CK(xb.alloc(n));
+      CK(bb.alloc(n));
+    }
+    if (partial.n < (size_t)kRedBlocks * (max_iter + 2)) CK(partial.alloc((size_t)kRedBlocks * (max_iter + 2)));
+    if (tmp.n < (size_t)max_iter + 2) {
+      CK(tmp.alloc(max_iter + 2));
+      CK(tmp2.alloc(max_iter + 2));
+    }
+    if (!scal.p) CK(scal.alloc(4));
+    if (!flag.p) CK(flag.alloc(1));
+    if (!pinned) CK(cudaMallocHost(&pinned, sizeof(double) * 1024));
+    return ALEFSI_OK;
+  }
+
+  int gmres(const double* b_in, double* x_out, double rel_tol, double abs_tol, int max_iter,
+            int host_ptrs, double* residuals, int* iterations, int* converged) {
+    if (!factorized) return fail(ALEFSI_ERR_STATE, "gmres before mg_factorize");
+    if (max_iter < 1 || max_iter > 510) return fail(ALEFSI_ERR_ARG, "max_iter must be in [1, 510]");
+    int rc = ensure_workspace(max_iter);
+    if (rc) return rc;
+    Level& F = fine();
+    const int64_t n = F.ndof();
+    const DevMatrix A = F.mat();
+    const double* b = b_in;
+    double* x = x_out;
+    if (host_ptrs) {
+      CK(cudaMemcpyAsync(bb.p, b_in, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+      b = bb.p;
+      x = xb.p;
+    }
+    launch_sumsq(b, n, partial.p, scal.p, stream);
+    CK(cudaMemcpyAsync(pinned, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    const double beta = std::sqrt(pinned[0]);
+    residuals[0] = beta;
+    *iterations = 0;
+    *converged = 1;
+    const double tol = std::max(rel_tol * beta, abs_tol);
+    if (beta == 0.0 || beta <= tol) {
+      CK(cudaMemsetAsync(x, 0, sizeof(double) * n, stream));
+      if (host_ptrs)
+        CK(cudaMemcpyAsync(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      return ALEFSI_OK;
+    }
+    const int m = max_iter;
+    std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1, 0.0);
+    auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
+    g[0] = beta;
+    launch_scale(b, V.p, beta, n, stream);
+    int k = 0;
+    double res = beta;
+    for (k = 0; k < m; ++k) {
+      double* vk = V.p + (size_t)k * n;
+      rc = apply(vk, z.p);
+      if (rc) return rc;
+      launch_spmv(A, z.p, nullptr, w.p, 0, stream);
+      // first classical Gram-Schmidt pass: tmp[0..k] = V w, tmp[k+1] = w.w
+      launch_multi_dot(k + 1, V.p, n, w.p, n, partial.p, tmp.p, nullptr, stream);
+      launch_multi_axpy(k + 1, V.p, n, tmp.p, w.p, n, partial.p, scal.p, nullptr, stream);
+      launch_arnoldi_finish(k, tmp.p, tmp2.p, tmp.p + k + 1, scal.p, flag.p, 0, stream);
+      // conditional second pass (device flag)
+      launch_multi_dot(k + 1, V.p, n, w.p, n, partial.p, tmp2.p, flag.p, stream);
+      launch_multi_axpy(k + 1, V.p, n, tmp2.p, w.p, n, partial.p, scal.p, flag.p, stream);
+      launch_arnoldi_finish(k, tmp.p, tmp2.p, tmp.p + k + 1, scal.p, flag.p, 1, stream);
+      launch_scale_copy(w.p, V.p + (size_t)(k + 1) * n, tmp.p + k + 1, n, stream);
+      kernel_launches += 14;
+      CK(cudaMemcpyAsync(pinned, tmp.p, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      for (int i = 0; i <= k + 1; ++i) Hat(i, k) = pinned[i];
+      // accumulated Givens rotations, then the new one (linsolve.py:88-98)
+      for (int i = 0; i < k; ++i) {
+        const double tt = cs[i] * Hat(i, k) + sn[i] * Hat(i + 1, k);
+        Hat(i + 1, k) = -sn[i] * Hat(i, k) + cs[i] * Hat(i + 1, k);
+        Hat(i, k) = tt;
+      }
+      const double r = std::hypot(Hat(k, k), Hat(k + 1, k));
+      cs[k] = Hat(k, k) / r;
+      sn[k] = Hat(k + 1, k) / r;
+      Hat(k, k) = r;
+      Hat(k + 1, k) = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      res = std::fabs(g[k + 1]);
+      residuals[k + 1] = res;
+      if (res <= tol) break;
+    }
+    const int its = std::min(k + 1, m);
+    *iterations = its;
+    // y = triu(H)^{-1} g, column-oriented back substitution
+    std::vector<double> y(g.begin(), g.begin() + its);
+    for (int j = its - 1; j >= 0; --j) {
+      y[j] /= Hat(j, j);
+      for (int i = 0; i < j; ++i) y[i] -= y[j] * Hat(i, j);
+    }
+    for (int i = 0; i < its; ++i) pinned[i] = y[i];
+    CK(cudaMemcpyAsync(tmp.p, pinned, sizeof(double) * its, cudaMemcpyHostToDevice, stream));
+    launch_combine(its, V.p, n, tmp.p, t.p, n, stream);
+    rc = apply(t.p, x);
+    if (rc) return rc;
+    if (host_ptrs)
+      CK(cudaMemcpyAsync(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (res > tol) {
+      *converged = 0;
+      return fail(ALEFSI_ERR_NOT_CONVERGED, "GMRES did not reach the tolerance");
+    }
+    return ALEFSI_OK;
+  }
+};
+
+}  // namespace alefsi
+
+using alefsi::MgHandle;
+using alefsi::fail;
+
+#define CKAPI(expr)                                                               \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess)                                                        \
+      return fail(ALEFSI_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+static MgHandle* H(alefsi_mg h) { return reinterpret_cast<MgHandle*>(h); }
+
+static int check_level(MgHandle* m, int level) {
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  if (level < 0 || level >= m->n_levels) return fail(ALEFSI_ERR_ARG, "level out of range");
+  return ALEFSI_OK;
+}
+
+extern "C" {
+
+int alefsi_device_count(int32_t* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  *count = (e == cudaSuccess) ? c : 0;
+  return ALEFSI_OK;
+}
+
+int alefsi_mg_create(int32_t n_levels, int32_t nc, int32_t nu_pre, int32_t nu_post, double omega,
+                     alefsi_mg* out) {
+  ALEFSI_TRY_BEGIN
+  if (n_levels < 1 || nc < 1 || nc > 4 || nu_pre < 0 || nu_post < 0)
+    return fail(ALEFSI_ERR_ARG, "mg_create: bad arguments");
+  auto* m = new MgHandle();
+  m->n_levels = n_levels;
+  m->nc = nc;
+  m->nu_pre = nu_pre;
+  m->nu_post = nu_post;
+  m->omega = omega;
+  m->lv.resize(n_levels);
+  for (auto& L : m->lv) L.nc = nc;
+  cudaError_t e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete m;
+    return fail(ALEFSI_ERR_CUDA, std::string("stream create: ") + cudaGetErrorString(e));
+  }
+  m->own_stream = true;
+  e = m->status.alloc(1);
+  if (e != cudaSuccess) {
+    delete m;
+    return fail(ALEFSI_ERR_CUDA, std::string("alloc: ") + cudaGetErrorString(e));
+  }
+  *out = reinterpret_cast<alefsi_mg>(m);
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_destroy(alefsi_mg h) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  if (m) {
+    cudaStreamSynchronize(m->stream);
+    delete m;
+  }
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_set_stream(alefsi_mg h, void* stream) {
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  cudaStreamSynchronize(m->stream);
+  if (m->own_stream) cudaStreamDestroy(m->stream);
+  m->stream = reinterpret_cast<cudaStream_t>(stream);
+  m->own_stream = false;
+  m->graph_valid = false;
+  return ALEFSI_OK;
+}
+
+int alefsi_mg_use_graph(alefsi_mg h, int32_t on) {
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  m->use_graph = on != 0;
+  m->graph_valid = false;
+  return ALEFSI_OK;
+}
+
+int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nnzb,
+                         const int64_t* indptr, const int32_t* indices, const double* data,
+                         int64_t nnz_pp, const int64_t* pp_indptr, const int32_t* pp_indices,
+                         const double* pp_data) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  const int nc = m->nc;
+  if (indptr[0] != 0 || indptr[n_nodes] != nnzb) return fail(ALEFSI_ERR_ARG, "bad indptr");
+  if (nnz_pp > 0 && (pp_indptr[0] != 0 || pp_indptr[n_nodes] != nnz_pp))
+    return fail(ALEFSI_ERR_ARG, "bad pp_indptr");
+  L.n_nodes = n_nodes;
+  L.nnzb = nnzb;
+  L.nnz_pp = nnz_pp;
+  CKAPI(L.indptr.upload(indptr, n_nodes + 1, m->stream));
+  CKAPI(L.indices.upload(indices, nnzb, m->stream));
+  CKAPI(L.data.upload(data, (size_t)nnzb * nc * nc, m->stream));
+  if (nnz_pp > 0) {
+    CKAPI(L.pp_indptr.upload(pp_indptr, n_nodes + 1, m->stream));
+    CKAPI(L.pp_indices.upload(pp_indices, nnz_pp, m->stream));
+    CKAPI(L.pp_data.upload(pp_data, nnz_pp, m->stream));
+  }
+  if (level == 0) {
+    const int64_t n0 = n_nodes * nc;
+    if (n0 > 20000) return fail(ALEFSI_ERR_ARG, "coarse level too large for a dense inverse");
+    L.host_dense.assign((size_t)n0 * n0, 0.0);
+    for (int64_t r = 0; r < n_nodes; ++r) {
+      for (int64_t s = indptr[r]; s < indptr[r + 1]; ++s) {
+        const int64_t c = indices[s];
+        for (int i = 0; i < nc; ++i)
+          for (int j = 0; j < nc; ++j)
+            L.host_dense[(size_t)(r * nc + i) * n0 + c * nc + j] +=
+                data[(size_t)s * nc * nc + i * nc + j];
+      }
+      if (nnz_pp > 0)
+        for (int64_t s = pp_indptr[r]; s < pp_indptr[r + 1]; ++s)
+          L.host_dense[(size_t)(r * nc) * n0 + (int64_t)pp_indices[s] * nc] += pp_data[s];
+    }
+  }
+  CKAPI(cudaStreamSynchronize(m->stream));
+  L.has_matrix = true;
+  m->factorized = false;
+  m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_set_patches(alefsi_mg h, int32_t level, int32_t n_groups,
+                          const int64_t* group_n_patches, const int32_t* group_nodes_per_patch,
+                          const int64_t* patch_nodes) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (L.n_nodes == 0) return fail(ALEFSI_ERR_STATE, "set_matrix before set_patches");
+  const int nc = m->nc;
+  L.groups.clear();
+  int64_t y_size = 0, flat_off = 0;
+  std::vector<int64_t> mult(L.n_nodes, 0);
+  // node -> (Y offset) gather entries in ascending global patch order
+  std::vector<int64_t> count(L.n_nodes + 1, 0);
+  for (int gi = 0; gi < n_groups; ++gi) {
+    const int npn = group_nodes_per_patch[gi];
+    const int64_t np_ = group_n_patches[gi];
+    for (int64_t s = 0; s < np_ * npn; ++s) {
+      const int64_t nd = patch_nodes[flat_off + s];
+      if (nd < 0 || nd >= L.n_nodes) return fail(ALEFSI_ERR_ARG, "patch node out of range");
+      count[nd + 1]++;
+    }
+    flat_off += np_ * npn;
+  }
+  for (int64_t i = 0; i < L.n_nodes; ++i) count[i + 1] += count[i];
+  std::vector<int64_t> goff(count[L.n_nodes]);
+  std::vector<int64_t> fill(count.begin(), count.end() - 1);
+  flat_off = 0;
+  for (int gi = 0; gi < n_groups; ++gi) {
+    auto g = std::make_unique<alefsi::Group>();
+    g->npn = group_nodes_per_patch[gi];
+    g->np = g->npn * nc;
+    g->ld = (g->np + 1) / 2 * 2;
+    g->n_patches = group_n_patches[gi];
+    g->y_offset = y_size;
+    std::vector<int32_t> nodes32((size_t)g->n_patches * g->npn);
+    for (int64_t p = 0; p < g->n_patches; ++p)
+      for (int a = 0; a < g->npn; ++a) {
+        const int64_t nd = patch_nodes[flat_off + p * g->npn + a];
+        nodes32[(size_t)p * g->npn + a] = (int32_t)nd;
+        goff[fill[nd]++] = y_size + p * g->ld + (int64_t)a * nc;
+      }
+    CKAPI(g->nodes.upload(nodes32.data(), nodes32.size(), m->stream));
+    CKAPI(cudaStreamSynchronize(m->stream));
+    flat_off += g->n_patches * g->npn;
+    y_size += g->n_patches * g->ld;
+    L.groups.push_back(std::move(g));
+  }
+  // weights 1 / multiplicity (linsolve.py:156-161)
+  std::vector<double> wts(L.n_nodes);
+  for (int64_t i = 0; i < L.n_nodes; ++i) {
+    const int64_t c = count[i + 1] - count[i];
+    wts[i] = 1.0 / (double)(c == 0 ? 1 : c);
+  }
+  CKAPI(L.Y.alloc(y_size));
+  CKAPI(L.gptr.upload(count.data(), count.size(), m->stream));
+  CKAPI(L.goff.upload(goff.data(), goff.size(), m->stream));
+  CKAPI(L.weight.upload(wts.data(), wts.size(), m->stream));
+  CKAPI(cudaStreamSynchronize(m->stream));
+  m->factorized = false;
+  m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_set_prolongation(alefsi_mg h, int32_t level, int64_t n_fine, int64_t n_coarse,
+                               int64_t nnz, const int64_t* indptr, const int32_t* indices,
+                               const double* vals) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  if (level == 0) return fail(ALEFSI_ERR_ARG, "level 0 has no prolongation");
+  auto& L = m->lv[level];
+  if (indptr[0] != 0 || indptr[n_fine] != nnz) return fail(ALEFSI_ERR_ARG, "bad P indptr");
+  CKAPI(L.P_ptr.upload(indptr, n_fine + 1, m->stream));
+  CKAPI(L.P_idx.upload(indices, nnz, m->stream));
+  CKAPI(L.P_val.upload(vals, nnz, m->stream));
+  // transpose (coarse rows, fine columns ascending)
+  std::vector<int64_t> rp(n_coarse + 1, 0);
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (indices[e] < 0 || indices[e] >= n_coarse) return fail(ALEFSI_ERR_ARG, "P column out of range");
+    rp[indices[e] + 1]++;
+  }
+  for (int64_t i = 0; i < n_coarse; ++i) rp[i + 1] += rp[i];
+  std::vector<int32_t> ri(nnz);
+  std::vector<double> rv(nnz);
+  std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+  for (int64_t r = 0; r < n_fine; ++r)
+    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) {
+      const int64_t pos = fill[indices[e]]++;
+      ri[pos] = (int32_t)r;
+      rv[pos] = vals[e];
+    }
+  CKAPI(L.R_ptr.upload(rp.data(), rp.size(), m->stream));
+  CKAPI(L.R_idx.upload(ri.data(), ri.size(), m->stream));
+  CKAPI(L.R_val.upload(rv.data(), rv.size(), m->stream));
+  CKAPI(cudaStreamSynchronize(m->stream));
+  L.n_coarse = n_coarse;
+  L.has_P = true;
+  m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_set_constrained(alefsi_mg h, int32_t level, const uint8_t* mask) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (L.n_nodes == 0) return fail(ALEFSI_ERR_STATE, "set_matrix before set_constrained");
+  CKAPI(L.constrained.upload(mask, L.ndof(), m->stream));
+  CKAPI(cudaStreamSynchronize(m->stream));
+  m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_factorize(alefsi_mg h) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  return m->factorize();
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_apply(alefsi_mg h, const double* b, double* z, int32_t host_ptrs) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  if (!host_ptrs) return m->apply(b, z);
+  const int64_t n = m->fine().ndof();
+  int rc = m->ensure_workspace(1);
+  if (rc) return rc;
+  CKAPI(cudaMemcpyAsync(m->bb.p, b, sizeof(double) * n, cudaMemcpyHostToDevice, m->stream));
+  rc = m->apply(m->bb.p, m->xb.p);
+  if (rc) return rc;
+  CKAPI(cudaMemcpyAsync(z, m->xb.p, sizeof(double) * n, cudaMemcpyDeviceToHost, m->stream));
+  CKAPI(cudaStreamSynchronize(m->stream));
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_spmv(alefsi_mg h, int32_t level, const double* x, const double* b, double* y) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  alefsi::launch_spmv(m->lv[level].mat(), x, b, y, b ? 1 : 0, m->stream);
+  CKAPI(cudaGetLastError());
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_vanka_sweep(alefsi_mg h, int32_t level, double* x, const double* b) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  if (!m->factorized) return fail(ALEFSI_ERR_STATE, "sweep before factorize");
+  if (level == 0) return fail(ALEFSI_ERR_ARG, "level 0 has no smoother");
+  m->sweep(m->lv[level], b, x, false);
+  CKAPI(cudaGetLastError());
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_restrict(alefsi_mg h, int32_t level, const double* r_fine, double* b_coarse) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  if (level == 0) return fail(ALEFSI_ERR_ARG, "level 0 has no coarser level");
+  auto& L = m->lv[level];
+  auto& C = m->lv[level - 1];
+  alefsi::launch_restrict(C.n_nodes, C.nc, L.R_ptr.p, L.R_idx.p, L.R_val.p, r_fine,
+                          C.constrained.p, b_coarse, m->stream);
+  CKAPI(cudaGetLastError());
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_prolong_add(alefsi_mg h, int32_t level, const double* x_coarse, double* x_fine) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  if (level == 0) return fail(ALEFSI_ERR_ARG, "level 0 has no coarser level");
+  auto& L = m->lv[level];
+  alefsi::launch_prolong_add(L.n_nodes, L.nc, L.P_ptr.p, L.P_idx.p, L.P_val.p, x_coarse,
+                             L.constrained.p, x_fine, m->stream);
+  CKAPI(cudaGetLastError());
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_coarse_solve(alefsi_mg h, const double* b, double* x) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  if (!m->factorized) return fail(ALEFSI_ERR_STATE, "coarse solve before factorize");
+  alefsi::launch_dense_matvec(m->lv[0].ndof(), m->coarse_inv.p, b, x, m->stream);
+  CKAPI(cudaGetLastError());
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_get_inverses(alefsi_mg h, int32_t level, int32_t group, double* out) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (group < 0 || group >= (int)L.groups.size()) return fail(ALEFSI_ERR_ARG, "bad group");
+  auto& g = *L.groups[group];
+  CKAPI(cudaMemcpyAsync(out, g.inv.p, sizeof(double) * g.inv.n, cudaMemcpyDeviceToHost,
+                        m->stream));
+  CKAPI(cudaStreamSynchronize(m->stream));
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+// info[0..7] = n_nodes, ndof, nnzb, nnz_pp, n_groups, y_size, inverse doubles, ld of group 0
+int alefsi_mg_info(alefsi_mg h, int32_t level, int64_t* info) {
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  int64_t inv = 0;
+  for (auto& g : L.groups) inv += g->n_patches * g->np * g->ld;
+  info[0] = L.n_nodes;
+  info[1] = L.ndof();
+  info[2] = L.nnzb;
+  info[3] = L.nnz_pp;
+  info[4] = (int64_t)L.groups.size();
+  info[5] = (int64_t)L.Y.n;
+  info[6] = inv;
+  info[7] = L.groups.empty() ? 0 : L.groups[0]->ld;
+  return ALEFSI_OK;
+}
+
+int alefsi_gmres(alefsi_mg h, const double* b, double* x, double rel_tol, double abs_tol,
+                 int32_t max_iter, int32_t host_ptrs, double* residuals, int32_t* iterations,
+                 int32_t* converged) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  int its = 0, conv = 0;
+  int rc = m->gmres(b, x, rel_tol, abs_tol, max_iter, host_ptrs, residuals, &its, &conv);
+  *iterations = its;
+  *converged = conv;
+  return rc;
+  ALEFSI_TRY_END
+}
+
+int alefsi_gmres_workspace(alefsi_mg h, int32_t max_iter) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  return m->ensure_workspace(max_iter);
+  ALEFSI_TRY_END
+}
+
+int alefsi_kernel_stats(alefsi_mg h, int64_t* launches) {
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  *launches = m->kernel_launches;
+  return ALEFSI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,213 @@
+"""Python handle over the device-resident multigrid hierarchy (C ABI).
+
+``DeviceMgSolver`` owns one ``alefsi_mg`` handle: per-level split block
+operators, Vanka patch tables and their inverses, Q2 transfer operators and
+the GMRES Krylov basis, all resident in HBM.  Vectors may be numpy arrays
+(host; copied in and out by the library, the end-to-end path) or CUDA
+tensors (device-resident, no copies).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+
+class SolverError(Exception):
+    """Raised when GMRES misses its tolerance or a patch is singular
+    (reference linsolve.py:25-28)."""
+
+    def __init__(self, message, stats=None):
+        super().__init__(message)
+        self.stats = stats
+
+
+@dataclass
+class KrylovStats:
+    iterations: int = 0
+    initial_residual: float = 0.0
+    final_residual: float = 0.0
+    elapsed: float = 0.0
+    converged: bool = True
+    residuals: list = field(default_factory=list)
+
+
+def _is_device(a):
+    return hasattr(a, "is_cuda") and a.is_cuda
+
+
+class DeviceMgSolver:
+    """V-cycle preconditioner + GMRES over a device level hierarchy.
+
+    ``levels`` are dicts with keys ``matrix`` (fem.SplitBlockMatrix),
+    ``patches`` (mesh.PatchSet; None on level 0), ``P`` (scipy CSR
+    prolongation from the coarser level; None on level 0) and
+    ``constrained`` (bool per dof)."""
+
+    def __init__(self, levels, nu_pre=2, nu_post=2, omega=0.8, use_graph=False, stream=None):
+        lib = _lib.load()
+        self.n_levels = len(levels)
+        self.nc = levels[0]["matrix"].nc
+        self.nu_pre, self.nu_post, self.omega = nu_pre, nu_post, omega
+        h = C.c_void_p()
+        _lib.call("alefsi_mg_create", self.n_levels, self.nc, nu_pre, nu_post, float(omega),
+                  C.byref(h))
+        self._h = h
+        self._lib = lib
+        if stream is not None:
+            _lib.call("alefsi_mg_set_stream", h, C.c_void_p(int(stream)))
+        self.ndofs = []
+        self._groups = {}
+        for l, lv in enumerate(levels):
+            self._set_level(l, lv)
+        _lib.call("alefsi_mg_use_graph", h, 1 if use_graph else 0)
+        self.factorize()
+
+    # -- setup ------------------------------------------------------------------
+    def _set_level(self, l, lv):
+        A = lv["matrix"]
+        p = A.pattern
+        _lib.call("alefsi_mg_set_matrix", self._h, l, p.n_nodes, p.nnzb,
+                  np.ascontiguousarray(p.indptr, dtype=np.int64),
+                  np.ascontiguousarray(p.indices, dtype=np.int32),
+                  np.ascontiguousarray(A.data, dtype=np.float64), p.nnz_pp,
+                  np.ascontiguousarray(p.pp_indptr, dtype=np.int64),
+                  np.ascontiguousarray(p.pp_indices, dtype=np.int32),
+                  np.ascontiguousarray(A.pp_data, dtype=np.float64))
+        self.ndofs.append(p.n_nodes * A.nc)
+        mask = np.ascontiguousarray(np.asarray(lv["constrained"]).reshape(-1), dtype=np.uint8)
+        _lib.call("alefsi_mg_set_constrained", self._h, l, mask)
+        if l == 0:
+            return
+        groups = [g for g, _ in lv["patches"].groups]
+        n_p = np.array([len(g) for g in groups], dtype=np.int64)
+        self._groups[l] = [(len(g), g.shape[1] * self.nc) for g in groups]
+        npn = np.array([g.shape[1] for g in groups], dtype=np.int32)
+        flat = np.ascontiguousarray(np.concatenate([g.reshape(-1) for g in groups]),
+                                    dtype=np.int64)
+        _lib.call("alefsi_mg_set_patches", self._h, l, len(groups), n_p, npn, flat)
+        P = lv["P"].tocsr()
+        _lib.call("alefsi_mg_set_prolongation", self._h, l, P.shape[0], P.shape[1], P.nnz,
+                  np.ascontiguousarray(P.indptr, dtype=np.int64),
+                  np.ascontiguousarray(P.indices, dtype=np.int32),
+                  np.ascontiguousarray(P.data, dtype=np.float64))
+
+    def factorize(self):
+        _lib.call("alefsi_mg_factorize", self._h)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.call("alefsi_mg_destroy", self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self, level):
+        out = np.zeros(8, dtype=np.int64)
+        _lib.call("alefsi_mg_info", self._h, level, out)
+        return dict(zip(["n_nodes", "ndof", "nnzb", "nnz_pp", "n_groups", "y_size",
+                         "inverse_doubles", "ld"], out.tolist()))
+
+    def kernel_launches(self):
+        out = np.zeros(1, dtype=np.int64)
+        _lib.call("alefsi_kernel_stats", self._h, out)
+        return int(out[0])
+
+    def inverses(self, level, group):
+        """Stored inverses of one patch group: (n_patches, np, np), row-major."""
+        n_p, npd = self._groups[level][group]
+        ld = npd + (npd % 2)
+        out = np.empty(n_p * npd * ld, dtype=np.float64)
+        _lib.call("alefsi_mg_get_inverses", self._h, level, group, out)
+        return out.reshape(n_p, npd, ld)[:, :, :npd].transpose(0, 2, 1)
+
+    # -- application --------------------------------------------------------------
+    def dot(self, b):
+        """One V-cycle (MgSolver.dot, reference linsolve.py:238-255)."""
+        if _is_device(b):
+            import torch
+            z = torch.empty_like(b)
+            _lib.call("alefsi_mg_apply", self._h, b, z, 0)
+            return z
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        z = np.empty_like(b)
+        _lib.call("alefsi_mg_apply", self._h, b, z, 1)
+        return z
+
+    __call__ = dot
+
+    def gmres(self, b, rel_tol=1e-4, abs_tol=0.0, max_iter=200, x_out=None, raise_on_fail=True):
+        """Right-preconditioned GMRES (reference linsolve.py:41-115)."""
+        import time
+        t0 = time.perf_counter()
+        res = np.zeros(max_iter + 1, dtype=np.float64)
+        its = np.zeros(1, dtype=np.int32)
+        conv = np.zeros(1, dtype=np.int32)
+        if _is_device(b):
+            import torch
+            x = x_out if x_out is not None else torch.empty_like(b)
+            host = 0
+        else:
+            b = np.ascontiguousarray(b, dtype=np.float64)
+            x = x_out if x_out is not None else np.empty_like(b)
+            host = 1
+        try:
+            _lib.call("alefsi_gmres", self._h, b, x, float(rel_tol), float(abs_tol), int(max_iter),
+                      host, res, its, conv)
+            err = None
+        except _lib.NativeError as exc:
+            if exc.code != 4:        # ALEFSI_ERR_NOT_CONVERGED
+                raise
+            err = exc
+        n = int(its[0])
+        stats = KrylovStats(iterations=n, initial_residual=float(res[0]),
+                            final_residual=float(res[n]), residuals=res[:n + 1].tolist(),
+                            converged=bool(conv[0]), elapsed=time.perf_counter() - t0)
+        if err is not None and raise_on_fail:
+            tol = max(rel_tol * stats.initial_residual, abs_tol)
+            raise SolverError(f"GMRES stalled at {stats.final_residual:.3e} (tol {tol:.3e}) "
+                              f"after {stats.iterations} iterations", stats)
+        return x, stats
+
+    # -- single kernels (parity tests, micro-benchmarks; device tensors) ------------
+    def spmv(self, level, x, b=None, y=None):
+        import torch
+        y = torch.empty_like(x) if y is None else y
+        _lib.call("alefsi_mg_spmv", self._h, level, x, b if b is not None else None, y)
+        return y
+
+    def sweep(self, level, x, b):
+        _lib.call("alefsi_mg_vanka_sweep", self._h, level, x, b)
+        return x
+
+    def restrict(self, level, r_fine, out):
+        _lib.call("alefsi_mg_restrict", self._h, level, r_fine, out)
+        return out
+
+    def prolong_add(self, level, x_coarse, x_fine):
+        _lib.call("alefsi_mg_prolong_add", self._h, level, x_coarse, x_fine)
+        return x_fine
+
+    def coarse_solve(self, b, x):
+        _lib.call("alefsi_mg_coarse_solve", self._h, b, x)
+        return x
+
+    def reserve(self, max_iter):
+        _lib.call("alefsi_gmres_workspace", self._h, int(max_iter))
+
+    # -- construction from a workload case -------------------------------------------
+    @classmethod
+    def from_case(cls, case, wl, **kw):
+        return cls(case.mg_levels(), nu_pre=wl.nu_pre, nu_post=wl.nu_post, omega=wl.omega, **kw)

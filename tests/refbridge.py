@@ -1,0 +1,59 @@
+"""Run the unmodified reference (``/root/reference/pkg/src/alefsi``) on a
+workload definition.  Only available in the build container, where the
+reference is mounted; tests using it are skipped elsewhere.  Also used by
+``tests/golden/make_golden.py`` to generate the committed fixtures."""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF_SRC = "/root/reference/pkg/src"
+AVAILABLE = os.path.isdir(os.path.join(REF_SRC, "alefsi"))
+
+
+def ref():
+    if not AVAILABLE:
+        raise RuntimeError("reference not mounted")
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import alefsi.mesh, alefsi.problem, alefsi.model, alefsi.newton, alefsi.linsolve  # noqa
+    import alefsi
+    return alefsi
+
+
+def ref_problem(wl):
+    """Reference FsiProblem for a workload (coarse arrays from box_mesh)."""
+    a = ref()
+    from paper_1904_02401_b200 import mesh as mm
+    c = mm.box_mesh(wl.lengths, wl.coarse_cells)
+    coarse = a.mesh.MeshLevel(c.dim, c.vertices, c.cells, c.cell_subdomain, c.facets)
+    h = a.mesh.build_hierarchy(coarse, wl.n_levels - 1)
+    for m in h.levels:
+        cen = m.vertices[m.cells].mean(axis=1)
+        inside = np.all((cen > np.asarray(wl.solid_lo)) & (cen < np.asarray(wl.solid_hi)), axis=1)
+        m.cell_subdomain = np.where(inside, a.mesh.SOLID, a.mesh.FLUID).astype(np.int8)
+    m0 = wl.materials()
+    mats = a.model.MaterialParams(rho_f=m0.rho_f, nu_f=m0.nu_f, rho_s=m0.rho_s, mu_s=m0.mu_s,
+                                  lam_s=m0.lam_s, body_force=m0.body_force)
+    flags = a.problem.FsiFlags(lps_dt=wl.dt)
+    return a.problem.FsiProblem(h, mats, flags)
+
+
+def ref_stack(wl, prob, U, Up):
+    a = ref()
+    fp, spt = wl.patch_strategies()
+    cfg = a.newton.LinearConfig(fluid_patches=fp, solid_patches=spt, nu_pre=wl.nu_pre,
+                                nu_post=wl.nu_post, omega=wl.omega, max_iter=wl.max_iter)
+    stack = a.newton.LinearStack(prob, cfg)
+    stack.build_momentum(U, Up, wl.dt, wl.theta)
+    return stack
+
+
+def ref_solve(wl, stack, b):
+    a = ref()
+    mg = stack.mom_mg
+    return a.linsolve.gmres(mg.levels[-1].matrix, b, mg, rel_tol=wl.rel_tol,
+                            max_iter=wl.max_iter)
