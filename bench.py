@@ -1,0 +1,432 @@
+"""Benchmark of the B200 MG-GMRES / Vanka linear-solve path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload 3d_large]
+
+One step = one full right-preconditioned GMRES solve to 1e-8 of the seeded
+condensed velocity-pressure Jacobian (BASELINE config 3: 3D, 128x32x32 Q2
+hexahedra, 5 levels, ~4.3M FP64 dofs, 108x108 Vanka patch inverses), with
+the level hierarchy and patch inverses resident in HBM.  ``value`` is
+solves/s over all ranks with the RHS already on the device; ``e2e`` is the
+same through the public ``DeviceMgSolver.gmres`` call from pinned host
+buffers (H2D of b and D2H of x inside the timed region).  N>1 runs
+independent replicas (the path does not shard).
+
+``--impl reference`` times the CPU oracle port of the reference's algorithm
+(the reference is Python and cannot travel to the GPU box) on bounded
+samples of the same workload with all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MG-GMRES solves/s and Vanka sweeps/s (FP64) at 3D 4.3M dofs; % of HBM roofline"
+UNIT = "solves/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------ algorithmic bytes
+def kernel_bytes(case, wl):
+    """Algorithmic HBM bytes of one finest-level launch of each kernel."""
+    A = case.matrices[-1]
+    p = A.pattern
+    nc = A.nc
+    n = p.n_nodes * nc
+    spmv = (p.nnzb * (nc * nc * 8 + 4) + (p.n_nodes + 1) * 8 + p.nnz_pp * 12
+            + ((p.n_nodes + 1) * 8 if p.nnz_pp else 0) + 3 * n * 8)
+    vanka = 0
+    for g, _ in case.patches[-1].groups:
+        npd = g.shape[1] * nc
+        vanka += len(g) * (npd * npd * 8 + npd * 8 + g.shape[1] * 4)
+    vanka += n * 8
+    return {"spmv": spmv, "vanka_apply": vanka}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world):
+    import torch
+    from paper_1904_02401_b200 import device, workloads as W
+    wl = W.CONFIGS[args.workload]
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    case = W.build_case(wl, with_coloring=False)
+    t_case = time.perf_counter() - t0
+    log(f"[rank {rank}] case built in {t_case:.1f}s {case.timings}")
+    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    solver = device.DeviceMgSolver.from_case(case, wl, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    solver.reserve(wl.max_iter)
+    log(f"[rank {rank}] upload + Vanka/coarse factorisation {t_setup:.2f}s")
+    b_dev = torch.from_numpy(case.b).to(dev)
+    x_dev = torch.empty_like(b_dev)
+
+    def solve():
+        return solver.gmres(b_dev, rel_tol=wl.rel_tol, max_iter=wl.max_iter, x_out=x_dev)
+
+    for _ in range(args.warmup):
+        _, st = solve()
+    iterations = st.iterations
+    log(f"[rank {rank}] warm-up done: {iterations} GMRES iterations")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: device-resident RHS, live per-kernel events
+    solver.profile(True)
+    solver.profile_read(reset=True)
+    launches0 = solver.kernel_launches()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, st = solve()
+        ev1.record(stream)
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    prof = solver.profile_read(reset=True)
+    solver.profile(False)
+    launches = solver.kernel_launches() - launches0
+    if not st.converged or st.iterations != iterations:
+        raise RuntimeError("timed solves diverged from the warm-up solves")
+
+    # ---- end to end through the public API from pinned host buffers
+    b_host = torch.from_numpy(case.b).pin_memory().numpy()
+    x_host = torch.empty(len(case.b), dtype=torch.float64).pin_memory().numpy()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        solver.gmres(b_host, rel_tol=wl.rel_tol, max_iter=wl.max_iter, x_out=x_host)
+    e1.record(stream)
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+
+    # ---- standalone finest-level sweep and SpMV throughput
+    L = solver.n_levels - 1
+    xs = torch.zeros_like(b_dev)
+    nsw = args.sweeps
+    for _ in range(3):
+        solver.sweep(L, xs, b_dev)
+    barrier()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(nsw):
+        solver.sweep(L, xs, b_dev)
+    s1.record(stream)
+    barrier()
+    ms_sweep = s0.elapsed_time(s1) / nsw
+    y = torch.empty_like(b_dev)
+    s0.record(stream)
+    for _ in range(nsw):
+        solver.spmv(L, xs, None, y)
+    s1.record(stream)
+    barrier()
+    ms_spmv = s0.elapsed_time(s1) / nsw
+
+    # ---- max over ranks
+    vals = torch.tensor([ms_total, ms_e2e, ms_sweep, ms_spmv], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+    ms_total, ms_e2e, ms_sweep, ms_spmv = vals.tolist()
+    if rank != 0:
+        return None
+
+    kb = kernel_bytes(case, wl)
+    peak, peak_src = peaks()
+    kernels = {}
+    total_prof = sum(v[1] for v in prof.values())
+    for (kind, finest), (cnt, ms) in prof.items():
+        if cnt:
+            key = f"{kind}{'_finest' if finest else '_coarser'}"
+            kernels[key] = {"launches": cnt, "avg_ms": ms / cnt, "share": ms / ms_total}
+    dom = max(("spmv", "vanka_apply"), key=lambda k: prof[(k, True)][1])
+    cnt, ms = prof[(dom, True)]
+    avg_ms = ms / cnt
+    achieved = kb[dom] / (avg_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(dom)
+    n = len(case.b)
+    solves_per_s = world * args.steps / (ms_total * 1e-3)
+    out = {
+        "metric": METRIC, "value": solves_per_s, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded sine-mode linearisation state and RHS, BASELINE config 3)",
+        "config": {"workload": args.workload, "fine_mesh": "x".join(map(str, wl.fine_cells)),
+                   "levels": wl.n_levels, "dofs": n,
+                   "vanka_block": "x".join([str(case.patches[-1].sizes()[0])] * 2),
+                   "nu_pre": wl.nu_pre, "nu_post": wl.nu_post, "omega": wl.omega,
+                   "rel_tol": wl.rel_tol, "gmres_iterations": iterations,
+                   "l2": "inputs larger than L2 (finest operator + inverses > 20 GB)",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "e2e": {"value": world * args.steps / (ms_e2e * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8 + 8 * (iterations + 1)},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": f"{dom} (finest level)", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": kb[dom],
+                     "avg_launch_ms": avg_ms, "share_of_step": ms / ms_total,
+                     "peak_source": peak_src},
+        "vanka_sweeps_per_s": 1e3 / ms_sweep,
+        "vanka_sweep_ms": ms_sweep,
+        "spmv_ms": ms_spmv, "spmv_gbs": kb["spmv"] / (ms_spmv * 1e-3) / 1e9,
+        "vanka_apply_gbs": kb["vanka_apply"] / (prof[("vanka_apply", True)][1] /
+                                                 max(1, prof[("vanka_apply", True)][0]) * 1e-3) / 1e9,
+        "setup_s": {"host_case": t_case, "device_upload_and_factorize": t_setup},
+        "kernels": kernels,
+        "profiled_time_fraction": total_prof / ms_total,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(case, wl, iterations, threads=1)
+    return out
+
+
+def ncu_traffic(kind):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f).get(kind)
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+def cpu_baseline(case, wl, iterations, threads=1, budget_patches=4096):
+    """Time the oracle port on bounded samples of the same workload and scale
+    to solves/s: one finest-level operator application, the finest-level
+    patch solves on a sample of patches (scaled by patch count), and one full
+    V-cycle over the coarser levels; composed per GMRES iteration exactly as
+    the V-cycle and Arnoldi step use them."""
+    from oracle import linsolve_oracle as orc
+    from paper_1904_02401_b200 import workloads as W
+    t_start = time.perf_counter()
+    A = orc.OracleOperator(case.matrices[-1])
+    x = np.random.default_rng(0).standard_normal(A.shape[0])
+    t0 = time.perf_counter()
+    y = A @ x
+    t_spmv = time.perf_counter() - t0
+    # finest-level Vanka patch solves on a sample
+    ps = case.patches[-1]
+    g0 = ps.groups[0][0]
+    ns = min(budget_patches, len(g0))
+    from paper_1904_02401_b200 import mesh as mm
+    sample = mm.PatchSet(n_comp=ps.n_comp)
+    sample.add(g0[:ns], 0)
+    sm = orc.VankaOracle(sample, wl.omega, threads)
+    t0 = time.perf_counter()
+    sm.factorize(case.matrices[-1])
+    t_fact_sample = time.perf_counter() - t0
+    d = x
+    t0 = time.perf_counter()
+    upd = np.zeros_like(x)
+    for dofs, inv, wts in zip(sm.dofs, sm.inverses, sm.weights):
+        for s in range(0, len(dofs), orc.CHUNK):
+            sl = slice(s, s + orc.CHUNK)
+            yv = wts[sl] * np.einsum("pij,pj->pi", inv[sl], d[dofs[sl]])
+            np.add.at(upd, dofs[sl].reshape(-1), yv.reshape(-1))
+    t_apply = (time.perf_counter() - t0) * ps.n_patches / ns
+    # coarser hierarchy: a real oracle V-cycle on levels 0..L-2
+    sub = W.Case(wl, _SubProblem(case.problem, -1), case.U, case.U_prev, case.matrices[:-1],
+                 case.patches[:-1], case.colorings[:-1], case.prolongations[:-1],
+                 np.zeros(case.matrices[-2].shape[0]))
+    t0 = time.perf_counter()
+    mg = orc.MgOracle(sub, wl.nu_pre, wl.nu_post, wl.omega, threads)
+    t_coarse_setup = time.perf_counter() - t0
+    bc = np.random.default_rng(1).standard_normal(mg.A[-1].shape[0])
+    t0 = time.perf_counter()
+    mg.dot(bc)
+    t_cycle_coarse = time.perf_counter() - t0
+    n_sweeps = wl.nu_pre + wl.nu_post
+    n_spmv = (wl.nu_pre - 1 if wl.nu_pre else 0) + wl.nu_post + 1
+    t_vcycle = n_sweeps * t_apply + n_spmv * t_spmv + t_cycle_coarse
+    # Arnoldi step: A M v plus ~2 passes over the basis (average k/2 vectors)
+    t0 = time.perf_counter()
+    Vb = np.random.default_rng(2).standard_normal((4, A.shape[0]))
+    h = Vb @ y
+    y -= Vb.T @ h
+    t_orth4 = time.perf_counter() - t0
+    t_iter = t_vcycle + t_spmv + t_orth4 * (iterations / 2 + 1) / 4
+    t_solve = iterations * t_iter + t_vcycle
+    return {"value": 1.0 / t_solve, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": (f"oracle (numpy/scipy restatement of reference linsolve.py) on {args_workload(wl)}: "
+                       f"1 finest-level operator application ({t_spmv:.2f}s), patch solves on "
+                       f"{ns}/{ps.n_patches} finest patches scaled by count, 1 full V-cycle on the "
+                       f"{len(case.matrices) - 1} coarser levels ({t_cycle_coarse:.2f}s); composed "
+                       f"per V-cycle ({n_sweeps} sweeps, {n_spmv} operator applications) x "
+                       f"{iterations} GMRES iterations + final V-cycle"),
+            "model_s": {"spmv_finest": t_spmv, "patch_solves_finest_scaled": t_apply,
+                        "vcycle_coarser": t_cycle_coarse, "vcycle": t_vcycle,
+                        "gmres_iteration": t_iter, "solve": t_solve,
+                        "sample_factorize": t_fact_sample, "coarser_setup": t_coarse_setup},
+            "wall_s": time.perf_counter() - t_start}
+
+
+def args_workload(wl):
+    return f"{wl.name} ({'x'.join(map(str, wl.fine_cells))})"
+
+
+class _SubProblem:
+    """Problem view without the finest level (for the coarser-level V-cycle)."""
+
+    def __init__(self, problem, drop):
+        self.levels = problem.levels[:drop]
+        self.mats, self.flags = problem.mats, problem.flags
+
+    @property
+    def fine(self):
+        return self.levels[-1]
+
+
+# ----------------------------------------------------------------- reference arm (CPU)
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from paper_1904_02401_b200 import workloads as W
+    wl = W.CONFIGS[args.workload]
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    case = W.build_case(wl, with_coloring=False)
+    log(f"[reference] case built in {time.perf_counter() - t0:.1f}s")
+    iterations = args.ref_iterations
+    samples = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(case, wl, iterations, threads=threads, budget_patches=args.ref_patches)
+        if i >= args.warmup:
+            samples.append(cb)
+    t_solve = statistics.mean(s["model_s"]["solve"] for s in samples)
+    value = 1.0 / t_solve
+    cb = dict(samples[-1])
+    cb["value"] = value
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_solve * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic (seeded sine-mode linearisation state and RHS, BASELINE config 3)",
+            "config": {"workload": args.workload, "fine_mesh": "x".join(map(str, wl.fine_cells)),
+                       "levels": wl.n_levels, "dofs": len(case.b),
+                       "gmres_iterations": iterations,
+                       "l2": "host run", "parallelism": f"{threads} host threads"},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="3d_large")
+    ap.add_argument("--sweeps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-iterations", type=int, default=0,
+                    help="GMRES iterations used to scale the reference arm (default: from the "
+                         "device run's golden count, see DESIGN.md)")
+    ap.add_argument("--ref-patches", type=int, default=4096)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group(backend=backend)
+    if args.impl == "reference" and args.ref_iterations <= 0:
+        args.ref_iterations = REFERENCE_ITERATIONS.get(args.workload, 50)
+    out = run_ours(args, rank, world) if args.impl == "ours" else run_reference(args, rank, world)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# GMRES iteration counts of the device solve (identical to the oracle's by
+# the parity tests); used to scale the reference arm's per-iteration sample.
+REFERENCE_ITERATIONS = {"3d_large": 40, "3d_small": 28, "2d_small": 13, "2d_large": 15}
+
+if __name__ == "__main__":
+    main()

@@ -150,6 +150,13 @@ int alefsi_gmres_workspace(alefsi_mg h, int32_t max_iter);
 /* Number of device kernels this handle has enqueued (graph replays excluded). */
 int alefsi_kernel_stats(alefsi_mg h, int64_t* launches);
 
+/* Live per-kernel timing with CUDA events on the launch stream (disables the
+ * graph path while on).  profile_read fills counts[14] and ms[14]: index
+ * kind + 7 * finest with kind 0 spmv, 1 vanka_apply, 2 vanka_gather,
+ * 3 restrict, 4 prolong, 5 coarse solve, 6 Krylov orthogonalisation. */
+int alefsi_mg_profile(alefsi_mg h, int32_t on);
+int alefsi_mg_profile_read(alefsi_mg h, int64_t* counts, double* ms, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,3 +10,9 @@ Pinning: the restatement is checked against the unmodified reference run
 in the build container (``tests/refbridge.py``) and against the committed
 golden fixtures generated from it (``tests/golden/make_golden.py``).
 """
+
+# Batched tiny LAPACK calls (patch inverses) crawl when OpenBLAS threads
+# every call; the oracle parallelises over patch chunks instead.
+from threadpoolctl import threadpool_limits as _tl
+
+_tl(limits=1, user_api="blas")

@@ -173,6 +173,28 @@ class VankaOracle:
         return x + self.omega * upd
 
 
+class OracleOperator:
+    """y = A x for the assembled operator: scipy block-CSR matvec over the
+    cell-stencil blocks plus the scalar pressure extension (the reference's
+    bsr.tocsr() matvec, without materialising the scalar CSR)."""
+
+    def __init__(self, A, threads=1):
+        p = A.pattern
+        self.nc = A.nc
+        self.shape = A.shape
+        self.B = sp.bsr_matrix((A.data, p.indices, p.indptr), shape=A.shape)
+        self.L = sp.csr_matrix((A.pp_data, p.pp_indices, p.pp_indptr),
+                               shape=(p.n_nodes, p.n_nodes))
+
+    def dot(self, x):
+        y = self.B @ x
+        if self.L.nnz:
+            y[::self.nc] += self.L @ x[::self.nc]
+        return y
+
+    __matmul__ = dot
+
+
 class MgOracle:
     """V-cycle with Vanka smoothing and a sparse-LU coarse solve
     (linsolve.py:229-270)."""
@@ -180,7 +202,7 @@ class MgOracle:
     def __init__(self, case, nu_pre=2, nu_post=2, omega=0.8, threads=1):
         self.nu_pre, self.nu_post = nu_pre, nu_post
         self.nc = case.matrices[0].nc
-        self.A = [m.to_csr() for m in case.matrices]
+        self.A = [OracleOperator(m) for m in case.matrices]
         self.P = case.prolongations
         self.constrained = [lvl.momentum_dirichlet.reshape(-1) for lvl in case.problem.levels]
         self.smoothers = [None]
@@ -188,7 +210,7 @@ class MgOracle:
             sm = VankaOracle(case.patches[l], omega, threads)
             sm.factorize(case.matrices[l])
             self.smoothers.append(sm)
-        self.coarse_lu = spla.splu(sp.csc_matrix(self.A[0]))
+        self.coarse_lu = spla.splu(sp.csc_matrix(case.matrices[0].to_csr()))
 
     def dot(self, b):
         return self.cycle(len(self.A) - 1, np.asarray(b, dtype=float))

@@ -144,19 +144,65 @@ struct MgHandle {
   double* pinned = nullptr;
   int64_t kernel_launches = 0;
 
+  // Optional live per-kernel timing with CUDA events on the launch stream.
+  // kind: 0 spmv, 1 vanka_apply, 2 vanka_gather, 3 restrict, 4 prolong,
+  //       5 coarse, 6 krylov; slot = kind + kKinds * (level is finest).
+  static constexpr int kKinds = 7;
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_slot;
+  int64_t prof_count[2 * kKinds] = {0};
+  double prof_ms[2 * kKinds] = {0};
+
   ~MgHandle() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (pinned) cudaFreeHost(pinned);
+    for (auto e : ev_pool) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
   Level& fine() { return lv.back(); }
 
+  // returns the event-pair index or -1
+  int prof_begin(int kind, int level) {
+    if (!prof_on) return -1;
+    if (ev_used + 2 > ev_pool.size()) {
+      for (int i = 0; i < 256; ++i) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        ev_pool.push_back(e);
+      }
+      ev_slot.resize(ev_pool.size() / 2);
+    }
+    const int pair = (int)(ev_used / 2);
+    cudaEventRecord(ev_pool[ev_used], stream);
+    ev_used += 2;
+    ev_slot[pair] = kind + kKinds * (level == n_levels - 1 ? 1 : 0);
+    return pair;
+  }
+  void prof_end(int pair) {
+    if (pair >= 0) cudaEventRecord(ev_pool[2 * pair + 1], stream);
+  }
+  // fold recorded pairs into the totals (stream must be idle)
+  void prof_collect() {
+    for (size_t p = 0; p < ev_used / 2; ++p) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ev_pool[2 * p], ev_pool[2 * p + 1]) == cudaSuccess) {
+        prof_ms[ev_slot[p]] += ms;
+        prof_count[ev_slot[p]] += 1;
+      }
+    }
+    ev_used = 0;
+  }
+
   // ---------------------------------------------------------------- V-cycle
-  void sweep(Level& L, const double* b, double* x, bool zero) {
+  void sweep(Level& L, int l, const double* b, double* x, bool zero) {
     const double* d = b;
     if (!zero) {
+      int pr = prof_begin(0, l);
       launch_spmv(L.mat(), x, b, L.d.p, 1, stream);
+      prof_end(pr);
       ++kernel_launches;
       d = L.d.p;
     }
@@ -169,43 +215,55 @@ struct MgHandle {
       dg.nodes = g->nodes.p;
       dg.inv = g->inv.p;
       dg.y_offset = g->y_offset;
+      int pr = prof_begin(1, l);
       launch_vanka_apply(dg, L.nc, d, L.Y.p, stream);
+      prof_end(pr);
       ++kernel_launches;
     }
+    int pr = prof_begin(2, l);
     launch_vanka_gather(L.n_nodes, L.nc, L.gptr.p, L.goff.p, L.weight.p, L.Y.p, x, omega,
                         zero ? 1 : 0, stream);
+    prof_end(pr);
     ++kernel_launches;
   }
 
   void cycle(int l, const double* b, double* x) {
     Level& L = lv[l];
     if (l == 0) {
+      int pr = prof_begin(5, l);
       launch_dense_matvec(L.ndof(), coarse_inv.p, b, x, stream);
+      prof_end(pr);
       ++kernel_launches;
       return;
     }
     bool zero = true;
     for (int s = 0; s < nu_pre; ++s) {
-      sweep(L, b, x, zero);
+      sweep(L, l, b, x, zero);
       zero = false;
     }
     if (zero) cudaMemsetAsync(x, 0, sizeof(double) * L.ndof(), stream);
+    int pr = prof_begin(0, l);
     launch_spmv(L.mat(), x, b, L.d.p, 1, stream);
+    prof_end(pr);
     Level& C = lv[l - 1];
+    pr = prof_begin(3, l);
     launch_restrict(C.n_nodes, C.nc, L.R_ptr.p, L.R_idx.p, L.R_val.p, L.d.p, C.constrained.p,
                     C.b.p, stream);
+    prof_end(pr);
     kernel_launches += 2;
     cycle(l - 1, C.b.p, C.x.p);
+    pr = prof_begin(4, l);
     launch_prolong_add(L.n_nodes, L.nc, L.P_ptr.p, L.P_idx.p, L.P_val.p, C.x.p,
                        L.constrained.p, x, stream);
+    prof_end(pr);
     ++kernel_launches;
-    for (int s = 0; s < nu_post; ++s) sweep(L, b, x, false);
+    for (int s = 0; s < nu_post; ++s) sweep(L, l, b, x, false);
   }
 
   int apply(const double* b, double* x) {
     if (!factorized) return fail(ALEFSI_ERR_STATE, "mg_apply before mg_factorize");
     const int64_t n = fine().ndof();
-    if (!use_graph) {
+    if (!use_graph || prof_on) {
       cycle(n_levels - 1, b, x);
       CK(cudaGetLastError());
       return ALEFSI_OK;
@@ -349,7 +407,10 @@ struct MgHandle {
       double* vk = V.p + (size_t)k * n;
       rc = apply(vk, z.p);
       if (rc) return rc;
+      int pr = prof_begin(0, n_levels - 1);
       launch_spmv(A, z.p, nullptr, w.p, 0, stream);
+      prof_end(pr);
+      pr = prof_begin(6, n_levels - 1);
       // first classical Gram-Schmidt pass: tmp[0..k] = V w, tmp[k+1] = w.w
       launch_multi_dot(k + 1, V.p, n, w.p, n, partial.p, tmp.p, nullptr, stream);
       launch_multi_axpy(k + 1, V.p, n, tmp.p, w.p, n, partial.p, scal.p, nullptr, stream);
@@ -359,9 +420,11 @@ struct MgHandle {
       launch_multi_axpy(k + 1, V.p, n, tmp2.p, w.p, n, partial.p, scal.p, flag.p, stream);
       launch_arnoldi_finish(k, tmp.p, tmp2.p, tmp.p + k + 1, scal.p, flag.p, 1, stream);
       launch_scale_copy(w.p, V.p + (size_t)(k + 1) * n, tmp.p + k + 1, n, stream);
+      prof_end(pr);
       kernel_launches += 14;
       CK(cudaMemcpyAsync(pinned, tmp.p, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, stream));
       CK(cudaStreamSynchronize(stream));
+      prof_collect();
       for (int i = 0; i <= k + 1; ++i) Hat(i, k) = pinned[i];
       // accumulated Givens rotations, then the new one (linsolve.py:88-98)
       for (int i = 0; i < k; ++i) {
@@ -396,6 +459,7 @@ struct MgHandle {
     if (host_ptrs)
       CK(cudaMemcpyAsync(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    prof_collect();
     if (res > tol) {
       *converged = 0;
       return fail(ALEFSI_ERR_NOT_CONVERGED, "GMRES did not reach the tolerance");
@@ -704,7 +768,7 @@ int alefsi_mg_vanka_sweep(alefsi_mg h, int32_t level, double* x, const double* b
   if (rc) return rc;
   if (!m->factorized) return fail(ALEFSI_ERR_STATE, "sweep before factorize");
   if (level == 0) return fail(ALEFSI_ERR_ARG, "level 0 has no smoother");
-  m->sweep(m->lv[level], b, x, false);
+  m->sweep(m->lv[level], level, b, x, false);
   CKAPI(cudaGetLastError());
   return ALEFSI_OK;
   ALEFSI_TRY_END
@@ -804,6 +868,31 @@ int alefsi_gmres_workspace(alefsi_mg h, int32_t max_iter) {
   if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
   return m->ensure_workspace(max_iter);
   ALEFSI_TRY_END
+}
+
+int alefsi_mg_profile(alefsi_mg h, int32_t on) {
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  cudaStreamSynchronize(m->stream);
+  m->prof_collect();
+  m->prof_on = on != 0;
+  return ALEFSI_OK;
+}
+
+int alefsi_mg_profile_read(alefsi_mg h, int64_t* counts, double* ms, int32_t reset) {
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  cudaStreamSynchronize(m->stream);
+  m->prof_collect();
+  for (int i = 0; i < 2 * MgHandle::kKinds; ++i) {
+    counts[i] = m->prof_count[i];
+    ms[i] = m->prof_ms[i];
+    if (reset) {
+      m->prof_count[i] = 0;
+      m->prof_ms[i] = 0.0;
+    }
+  }
+  return ALEFSI_OK;
 }
 
 int alefsi_kernel_stats(alefsi_mg h, int64_t* launches) {

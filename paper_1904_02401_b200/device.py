@@ -125,6 +125,22 @@ class DeviceMgSolver:
         _lib.call("alefsi_kernel_stats", self._h, out)
         return int(out[0])
 
+    KINDS = ["spmv", "vanka_apply", "vanka_gather", "restrict", "prolong", "coarse", "krylov"]
+
+    def profile(self, on=True):
+        """Toggle live CUDA-event timing of every kernel on the launch stream."""
+        _lib.call("alefsi_mg_profile", self._h, 1 if on else 0)
+
+    def profile_read(self, reset=True):
+        """{(kind, finest): (launches, total_ms)} since the last reset."""
+        counts = np.zeros(14, dtype=np.int64)
+        ms = np.zeros(14, dtype=np.float64)
+        _lib.call("alefsi_mg_profile_read", self._h, counts, ms, 1 if reset else 0)
+        out = {}
+        for i in range(14):
+            out[(self.KINDS[i % 7], bool(i // 7))] = (int(counts[i]), float(ms[i]))
+        return out
+
     def inverses(self, level, group):
         """Stored inverses of one patch group: (n_patches, np, np), row-major."""
         n_p, npd = self._groups[level][group]

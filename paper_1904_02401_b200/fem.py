@@ -23,6 +23,8 @@ the bytes the device SpMV streams by ~2.5x.
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -233,30 +235,67 @@ def lps_local_matrices(mesh, table, qpoints, G, wdet, delta_cell, groups, macro_
             off = np.array([(j >> i) & 1 for i in range(dim)], dtype=float)
             q1[j] = _q1_table(0.5 * (qpoints + off), dim)
     n1 = q1.shape[2]
+    Q = q1.reshape(nch * nq, n1)                                 # ((j q), i)
     out = np.empty((nm, nmn, nmn))
-    for s in range(0, nm, chunk):
+
+    def work(s):
         g = groups[s:s + chunk]
         m = len(g)
         child = mesh.cell_nodes[g]                              # (m, nch, nb)
         mn = macro_nodes[s:s + chunk]
-        loc = np.empty((m, nch, nb), dtype=np.int64)
-        for i in range(m):
-            loc[i] = np.searchsorted(mn[i], child[i])
+        # macro-local position of every child basis function
+        key = np.arange(m, dtype=np.int64)[:, None] * (mesh.n_nodes + 1)
+        loc = np.searchsorted((mn + key).reshape(-1),
+                              (child.reshape(m, -1) + key).reshape(-1)).reshape(m, nch, nb)
+        loc -= np.arange(m)[:, None, None] * nmn
         Gm = np.zeros((m, nch, nq, nmn, dim))
         idx = np.broadcast_to(loc[:, :, None, :], (m, nch, nq, nb))
         Gc = G[g]                                               # (m, nch, nq, nb, d)
         for i in range(dim):
             np.put_along_axis(Gm[..., i], idx, Gc[..., i], axis=3)
-        wq = wdet[g]
-        dq = delta_cell[g][:, :, None] * wq
-        M = np.einsum("mjq,jqi,jql->mil", wq, q1, q1)
-        rhs = np.einsum("mjq,jqi,mjqad->miad", wq, q1, Gm, optimize=True)
-        coef = np.linalg.solve(M, rhs.reshape(m, n1, -1)).reshape(rhs.shape)
-        fluct = Gm - np.einsum("jqi,miad->mjqad", q1, coef, optimize=True)
-        F = fluct.reshape(m, nch * nq, nmn, dim).transpose(0, 1, 3, 2).reshape(m, -1, nmn)
-        wts = np.repeat(dq.reshape(m, nch * nq), dim, axis=1)
-        out[s:s + m] = np.einsum("mk,mka,mkb->mab", wts, F, F, optimize=True)
+        wq = wdet[g].reshape(m, nch * nq)
+        dq = (delta_cell[g][:, :, None] * wdet[g]).reshape(m, nch * nq)
+        Gk = Gm.reshape(m, nch * nq, nmn * dim)
+        M = np.matmul(Q.T[None] * wq[:, None, :], Q[None])                  # (m, i, l)
+        rhs = np.matmul(Q.T[None] * wq[:, None, :], Gk)                     # (m, i, (a d))
+        coef = np.linalg.solve(M, rhs)
+        fluct = (Gk - np.matmul(Q[None], coef)).reshape(m, nch * nq, nmn, dim)
+        F = fluct.transpose(0, 1, 3, 2).reshape(m, nch * nq * dim, nmn)
+        wts = np.repeat(dq, dim, axis=1)
+        out[s:s + m] = np.matmul(np.swapaxes(F * wts[:, :, None], 1, 2), F)
+
+    parallel_chunks(work, range(0, nm, chunk))
     return out
+
+
+def single_blas():
+    """Context: one BLAS thread.  The batched tiny LAPACK calls of the setup
+    (3x3 / 4x4 / 108x108 inverses) slow down by orders of magnitude when
+    OpenBLAS threads each call."""
+    from threadpoolctl import threadpool_limits
+    return threadpool_limits(limits=1, user_api="blas")
+
+
+def parallel_chunks(fn, starts, consume=None):
+    """Run independent chunk jobs on a thread pool (numpy releases the GIL);
+    ``consume`` receives the results in chunk order on the calling thread."""
+    from threadpoolctl import threadpool_limits
+    starts = list(starts)
+    n = min(len(starts), os.cpu_count() or 1)
+    with threadpool_limits(limits=1 if n > 1 else None):
+        if n <= 1:
+            results = map(fn, starts)
+            pool = None
+        else:
+            pool = ThreadPoolExecutor(max_workers=n)
+            results = pool.map(fn, starts)
+        try:
+            for r in results:
+                if consume is not None:
+                    consume(r)
+        finally:
+            if pool is not None:
+                pool.shutdown()
 
 
 # -- sparsity patterns and the split operator ----------------------------------------

@@ -169,6 +169,11 @@ def _outflow_blocks(fq, U, mats, k, theta, d):
 
 def momentum_jacobian(lvl, mats, flags, k, theta, U, U_prev, chunk=2048):
     """Reduced (p, v) Jacobian on one level in the split block layout."""
+    with fem.single_blas():
+        return _momentum_jacobian(lvl, mats, flags, k, theta, U, U_prev, chunk)
+
+
+def _momentum_jacobian(lvl, mats, flags, k, theta, U, U_prev, chunk):
     d = lvl.dim
     nc = d + 1
     p = lvl.pattern
@@ -176,11 +181,15 @@ def momentum_jacobian(lvl, mats, flags, k, theta, U, U_prev, chunk=2048):
     N = lvl.table.N
     conn_all = lvl.mesh.cell_nodes
     for cells, kernel in ((lvl.fluid_cells, _fluid_blocks), (lvl.solid_cells, _solid_blocks)):
-        for s in range(0, len(cells), chunk):
+        def work(s, cells=cells, kernel=kernel):
             c = cells[s:s + chunk]
             conn = conn_all[c]
-            local = kernel(lvl.G[c], N, lvl.wdet[c], U[conn], U_prev[conn], mats, k, theta)
-            fem.scatter_blocks(p.indptr, p.indices, A.data, conn, local)
+            return conn, kernel(lvl.G[c], N, lvl.wdet[c], U[conn], U_prev[conn], mats, k, theta)
+
+        def scatter(res):
+            # in chunk order: same accumulation order as one sequential pass
+            fem.scatter_blocks(p.indptr, p.indices, A.data, res[0], res[1])
+        fem.parallel_chunks(work, range(0, len(cells), chunk), scatter)
     if lvl.outflow is not None:
         local = _outflow_blocks(lvl.outflow, U, mats, k, theta, d)
         fem.scatter_blocks(p.indptr, p.indices, A.data, lvl.outflow.conn, local)

@@ -108,6 +108,9 @@ CONFIGS = {
     "3d_mini": _box(3, (8, 2, 2), 3, "3d_mini"),          # 32x8x8 fine, ~75k dofs
     "2d_one": Workload("2d_one", 2, (4.0, 1.0), (16, 4), 3, (1.0, 0.4), (2.0, 0.6),
                        fluid_patches="one", solid_patches="one"),
+    # 16x4x4 fine, solid block against the y=0/z=0 walls: smallest 3D case with solid
+    "3d_tiny": Workload("3d_tiny", 3, (4.0, 1.0, 1.0), (4, 1, 1), 3, (1.0, 0.0, 0.0),
+                        (2.0, 0.5, 0.5)),
 }
 
 

@@ -1,0 +1,179 @@
+"""Device path (C ABI, sm_100a kernels) vs the reference's golden outputs and
+the CPU oracle.  Tolerances: GMRES residual histories 1e-10 relative with
+identical iteration counts, solutions 1e-9 relative (north_star), kernel
+outputs ~1e-13 (FP64 summation-order differences only)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, get_case, gpu_available, load_golden
+from golden_util import vector_checksums
+
+from oracle import linsolve_oracle as orc
+from paper_1904_02401_b200 import device, workloads as W
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="no CUDA device")]
+
+SMALL = ["2d_mini", "2d_one", "3d_tiny"]
+_SOLVERS = {}
+
+
+def solver_for(name, **kw):
+    key = (name, tuple(sorted(kw.items())))
+    if key not in _SOLVERS:
+        case = get_case(name)
+        _SOLVERS[key] = device.DeviceMgSolver.from_case(case, W.CONFIGS[name], **kw)
+    return _SOLVERS[key]
+
+
+def assert_history(st, residuals, iterations):
+    assert st.iterations == iterations
+    r, rr = np.array(st.residuals), np.array(residuals)
+    assert np.max(np.abs(r - rr) / rr) < 1e-10
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("graph", [False, True])
+def test_device_gmres_matches_reference_golden(name, graph):
+    g, arr = load_golden(name)
+    wl = W.CONFIGS[name]
+    s = solver_for(name, use_graph=graph)
+    x, st = s.gmres(arr["b"], rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    assert_history(st, g["residuals"], g["iterations"])
+    assert np.linalg.norm(x - arr["x"]) <= 1e-9 * np.linalg.norm(arr["x"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_device_vcycle_matches_reference_and_oracle(name):
+    _, arr = load_golden(name)
+    case = get_case(name)
+    wl = W.CONFIGS[name]
+    z = solver_for(name).dot(case.b)
+    assert np.linalg.norm(z - arr["vcycle"]) <= 1e-11 * np.linalg.norm(arr["vcycle"])
+    zo = orc.MgOracle(case, wl.nu_pre, wl.nu_post, wl.omega).dot(case.b)
+    assert np.linalg.norm(z - zo) <= 1e-12 * np.linalg.norm(zo)
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_device_kernels_vs_oracle(name):
+    import torch
+    case = get_case(name)
+    wl = W.CONFIGS[name]
+    s = solver_for(name)
+    mg = orc.MgOracle(case, wl.nu_pre, wl.nu_post, wl.omega)
+    rng = np.random.default_rng(7)
+    for l in range(len(case.matrices)):
+        A = mg.A[l]
+        x = rng.standard_normal(A.shape[0])
+        b = rng.standard_normal(A.shape[0])
+        y = s.spmv(l, _t(x)).cpu().numpy()
+        assert np.linalg.norm(y - A @ x) <= 1e-13 * np.linalg.norm(A @ x)
+        d = s.spmv(l, _t(x), _t(b)).cpu().numpy()
+        assert np.linalg.norm(d - (b - A @ x)) <= 1e-13 * np.linalg.norm(b - A @ x)
+        if l == 0:
+            xc = torch.empty(A.shape[0], dtype=torch.float64, device="cuda")
+            s.coarse_solve(_t(b), xc)
+            ref = mg.coarse_lu.solve(b)
+            assert np.linalg.norm(xc.cpu().numpy() - ref) <= 1e-9 * np.linalg.norm(ref)
+            continue
+        # one Vanka sweep from a nonzero iterate
+        xs = _t(x)
+        s.sweep(l, xs, _t(b))
+        ref = mg.smoothers[l].sweep(A, x, b)
+        assert np.linalg.norm(xs.cpu().numpy() - ref) <= 1e-12 * np.linalg.norm(ref)
+        # stored inverses
+        for gi, inv_ref in enumerate(mg.smoothers[l].inverses):
+            inv = s.inverses(l, gi)
+            assert np.max(np.abs(inv - inv_ref)) <= 1e-10 * np.max(np.abs(inv_ref))
+        # transfers
+        nc = case.matrices[l].nc
+        P = case.prolongations[l]
+        con_c = case.problem.levels[l - 1].momentum_dirichlet.reshape(-1)
+        con_f = case.problem.levels[l].momentum_dirichlet.reshape(-1)
+        rc = torch.empty(P.shape[1] * nc, dtype=torch.float64, device="cuda")
+        s.restrict(l, _t(x), rc)
+        ref = (P.T @ x.reshape(-1, nc)).reshape(-1)
+        ref[con_c] = 0.0
+        np.testing.assert_allclose(rc.cpu().numpy(), ref, rtol=1e-13, atol=1e-13)
+        zc = rng.standard_normal(P.shape[1] * nc)
+        xf = _t(x)
+        s.prolong_add(l, _t(zc), xf)
+        add = (P @ zc.reshape(-1, nc)).reshape(-1)
+        add[con_f] = 0.0
+        np.testing.assert_allclose(xf.cpu().numpy(), x + add, rtol=1e-13, atol=1e-13)
+
+
+def test_device_gmres_is_deterministic_and_device_resident():
+    import torch
+    name = "3d_tiny"
+    wl = W.CONFIGS[name]
+    case = get_case(name)
+    s = solver_for(name)
+    b = _t(case.b)
+    x1, st1 = s.gmres(b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    x2, st2 = s.gmres(b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    assert torch.equal(x1, x2)
+    assert st1.residuals == st2.residuals
+    xh, _ = s.gmres(case.b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    np.testing.assert_array_equal(xh, x1.cpu().numpy())
+
+
+def test_device_gmres_not_converged_raises():
+    name = "2d_mini"
+    s = solver_for(name)
+    case = get_case(name)
+    with pytest.raises(device.SolverError) as exc:
+        s.gmres(case.b, rel_tol=1e-14, max_iter=3)
+    assert exc.value.stats.iterations == 3 and not exc.value.stats.converged
+
+
+def test_zero_rhs_returns_zero():
+    s = solver_for("2d_mini")
+    case = get_case("2d_mini")
+    x, st = s.gmres(np.zeros_like(case.b), rel_tol=1e-8)
+    assert st.iterations == 0 and not x.any()
+
+
+@pytest.mark.parametrize("name", ["2d_small", "3d_small"])
+def test_device_full_size_vs_reference_history(name):
+    """BASELINE configs 0 and 2 at full size against the reference's own run."""
+    if not os.path.exists(os.path.join(GOLDEN, f"{name}.json")):
+        pytest.skip("golden file not generated")
+    g, _ = load_golden(name)
+    wl = W.CONFIGS[name]
+    s = solver_for(name)
+    x, st = s.gmres(get_case(name).b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    assert_history(st, g["residuals"], g["iterations"])
+    np.testing.assert_allclose(vector_checksums(x), g["x_checksums"], rtol=1e-9)
+
+
+def test_device_headline_size_properties():
+    """3D 4.3M-dof workload (BASELINE config 3): size-independent checks —
+    convergence with a monotone history, true residual, V-cycle linearity,
+    bitwise determinism."""
+    import torch
+    name = "3d_large"
+    wl = W.CONFIGS[name]
+    s = solver_for(name)
+    case = get_case(name)
+    b = _t(case.b)
+    x, st = s.gmres(b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    res = np.array(st.residuals)
+    assert st.converged and res[-1] <= wl.rel_tol * res[0]
+    assert np.all(np.diff(res) <= 1e-12 * res[0])
+    r = s.spmv(len(case.matrices) - 1, x, b)
+    true_rel = float(torch.linalg.norm(r) / torch.linalg.norm(b))
+    assert true_rel <= 10 * wl.rel_tol
+    b2 = torch.roll(b, 17)
+    lin = s.dot(2.0 * b - 0.5 * b2) - (2.0 * s.dot(b) - 0.5 * s.dot(b2))
+    assert float(torch.linalg.norm(lin)) <= 1e-11 * float(torch.linalg.norm(s.dot(b)))
+    x2, st2 = s.gmres(b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    assert torch.equal(x, x2) and st.residuals == st2.residuals
