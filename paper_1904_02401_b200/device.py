@@ -58,6 +58,15 @@ class DeviceMgSolver:
                   C.byref(h))
         self._h = h
         self._lib = lib
+        if stream is None:
+            # enqueue on torch's current stream so device tensors passed in are
+            # ordered after the work that produced them
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream().cuda_stream
+            except ImportError:
+                pass
         if stream is not None:
             _lib.call("alefsi_mg_set_stream", h, C.c_void_p(int(stream)))
         self.ndofs = []

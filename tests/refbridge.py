@@ -31,9 +31,10 @@ def ref_problem(wl):
     c = mm.box_mesh(wl.lengths, wl.coarse_cells)
     coarse = a.mesh.MeshLevel(c.dim, c.vertices, c.cells, c.cell_subdomain, c.facets)
     h = a.mesh.build_hierarchy(coarse, wl.n_levels - 1)
+    lo, hi = wl.solid_box()
     for m in h.levels:
         cen = m.vertices[m.cells].mean(axis=1)
-        inside = np.all((cen > np.asarray(wl.solid_lo)) & (cen < np.asarray(wl.solid_hi)), axis=1)
+        inside = np.all((cen > np.asarray(lo)) & (cen < np.asarray(hi)), axis=1)
         m.cell_subdomain = np.where(inside, a.mesh.SOLID, a.mesh.FLUID).astype(np.int8)
     m0 = wl.materials()
     mats = a.model.MaterialParams(rho_f=m0.rho_f, nu_f=m0.nu_f, rho_s=m0.rho_s, mu_s=m0.mu_s,
