@@ -136,6 +136,9 @@ struct MgHandle {
   bool use_graph = false;
   bool graph_valid = false;
   cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  cudaEvent_t cap_in = nullptr, cap_out = nullptr;
+  int64_t graph_kernels = 0;
   DevBuf<double> g_in, g_out;
   // GMRES workspace
   int v_cap = 0;
@@ -157,6 +160,9 @@ struct MgHandle {
 
   ~MgHandle() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (cap_in) cudaEventDestroy(cap_in);
+    if (cap_out) cudaEventDestroy(cap_out);
     if (pinned) cudaFreeHost(pinned);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -268,20 +274,46 @@ struct MgHandle {
       CK(cudaGetLastError());
       return ALEFSI_OK;
     }
+    // The V-cycle is captured and replayed on a private stream (the caller's
+    // stream may be the legacy default stream, which cannot be captured),
+    // ordered against the caller's stream with events.
+    if (!cap_stream) {
+      CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&cap_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&cap_out, cudaEventDisableTiming));
+    }
     if (!graph_valid) {
       CK(g_in.alloc(n));
       CK(g_out.alloc(n));
+      if (graph_exec) {
+        cudaGraphExecDestroy(graph_exec);
+        graph_exec = nullptr;
+      }
       cudaGraph_t graph;
-      CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-      cycle(n_levels - 1, g_in.p, g_out.p);
-      CK(cudaStreamEndCapture(stream, &graph));
+      cudaStream_t user = stream;
+      stream = cap_stream;
+      const int64_t before = kernel_launches;
+      cudaError_t e = cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        cycle(n_levels - 1, g_in.p, g_out.p);
+        e = cudaStreamEndCapture(stream, &graph);
+      }
+      stream = user;
+      CK(e);
+      graph_kernels = kernel_launches - before;
+      kernel_launches = before;
       CK(cudaGraphInstantiate(&graph_exec, graph, 0));
       cudaGraphDestroy(graph);
       graph_valid = true;
     }
     CK(cudaMemcpyAsync(g_in.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
-    CK(cudaGraphLaunch(graph_exec, stream));
+    CK(cudaEventRecord(cap_in, stream));
+    CK(cudaStreamWaitEvent(cap_stream, cap_in, 0));
+    CK(cudaGraphLaunch(graph_exec, cap_stream));
+    CK(cudaEventRecord(cap_out, cap_stream));
+    CK(cudaStreamWaitEvent(stream, cap_out, 0));
     CK(cudaMemcpyAsync(x, g_out.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, stream));
+    kernel_launches += graph_kernels;
     return ALEFSI_OK;
   }
 
