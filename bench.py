@@ -99,6 +99,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def max_over_ranks(values, world, device=None):
+    """Element-wise max of per-rank timings (replicas: the slowest rank sets
+    the whole-job time)."""
+    import torch
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def whole_job_rate(units_per_rank, world, ms):
+    """Units processed by all ranks / max-over-ranks time."""
+    return world * units_per_rank / (ms * 1e-3)
+
+
 # ------------------------------------------------------------------------ algorithmic bytes
 def kernel_bytes(case, wl):
     """Algorithmic HBM bytes of one finest-level launch of each kernel."""
@@ -206,10 +222,8 @@ def run_ours(args, rank, world):
     ms_spmv = s0.elapsed_time(s1) / nsw
 
     # ---- max over ranks
-    vals = torch.tensor([ms_total, ms_e2e, ms_sweep, ms_spmv], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
-    ms_total, ms_e2e, ms_sweep, ms_spmv = vals.tolist()
+    ms_total, ms_e2e, ms_sweep, ms_spmv = max_over_ranks(
+        [ms_total, ms_e2e, ms_sweep, ms_spmv], world, dev)
     if rank != 0:
         return None
 
@@ -231,7 +245,7 @@ def run_ours(args, rank, world):
     achieved = kb[dom] / (avg_ms * 1e-3) / 1e9
     traffic = ncu_traffic(dom)
     n = len(case.b)
-    solves_per_s = world * args.steps / (ms_total * 1e-3)
+    solves_per_s = whole_job_rate(args.steps, world, ms_total)
     out = {
         "metric": METRIC, "value": solves_per_s, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,

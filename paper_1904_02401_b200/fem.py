@@ -414,6 +414,31 @@ class SplitBlockMatrix:
     def dot(self, x):
         return self.to_csr() @ x
 
+    @classmethod
+    def from_union(cls, n_nodes, indptr, indices, data):
+        """Split a reference-layout operator (BlockPattern indptr/indices,
+        data (nnzb, nc, nc)) by value: blocks whose entries other than (0,0)
+        are all zero (the LPS macro couplings) become scalar pp entries;
+        diagonal blocks always stay blocks."""
+        indptr = np.asarray(indptr, dtype=np.int64)
+        indices = np.asarray(indices)
+        rows = np.repeat(np.arange(n_nodes, dtype=np.int64), np.diff(indptr))
+        off = np.array(data, copy=True)
+        off[:, 0, 0] = 0.0
+        cell = np.any(off.reshape(len(data), -1) != 0.0, axis=1) | (rows == indices)
+
+        def csr(mask):
+            ptr = np.concatenate([[0], np.cumsum(np.bincount(rows[mask], minlength=n_nodes))])
+            return ptr.astype(np.int64), indices[mask].astype(np.int32)
+        ip, ix = csr(cell)
+        pp, px = csr(~cell)
+        key = rows[cell] * n_nodes + ix
+        diag = np.searchsorted(key, np.arange(n_nodes, dtype=np.int64) * (n_nodes + 1))
+        pat = SplitPattern(n_nodes, ip, ix, pp, px, indptr, indices.astype(np.int32),
+                           np.zeros(0, dtype=np.int64), np.zeros(0, dtype=np.int64),
+                           diag.astype(np.int64))
+        return cls(pat, np.ascontiguousarray(data[cell]), np.ascontiguousarray(data[~cell, 0, 0]))
+
     def copy(self):
         return SplitBlockMatrix(self.pattern, self.data.copy(), self.pp_data.copy())
 

@@ -111,6 +111,22 @@ def test_device_kernels_vs_oracle(name):
         np.testing.assert_allclose(xf.cpu().numpy(), x + add, rtol=1e-13, atol=1e-13)
 
 
+def test_reference_named_linear_stack_api():
+    """newton.LinearStack / linsolve.gmres mirror the reference entry points
+    (build_momentum + solve_momentum) and reproduce the golden history."""
+    from paper_1904_02401_b200 import newton
+    g, arr = load_golden("2d_mini")
+    wl = W.CONFIGS["2d_mini"]
+    case = get_case("2d_mini")
+    fs, ss = wl.patch_strategies()
+    cfg = newton.LinearConfig(momentum_rel_tol=wl.rel_tol, fluid_patches=fs, solid_patches=ss)
+    stack = newton.LinearStack(case.problem, cfg)
+    stack.build_momentum(case.U, case.U_prev, wl.dt, wl.theta)
+    x, st = stack.solve_momentum(arr["b"])
+    assert_history(st, g["residuals"], g["iterations"])
+    assert np.linalg.norm(x - arr["x"]) <= 1e-9 * np.linalg.norm(arr["x"])
+
+
 def test_device_gmres_is_deterministic_and_device_resident():
     import torch
     name = "3d_tiny"

@@ -97,6 +97,21 @@ def test_split_layout_reencodes_union_layout():
             assert not blk.any()
 
 
+@pytest.mark.parametrize("name", ["2d_mini", "3d_tiny"])
+def test_value_split_of_reference_layout_is_exact(name):
+    """INTEGRATION.md's hand-over: a reference-layout (union pattern) operator
+    split by value gives the same operator."""
+    case = get_case(name)
+    for l, lvl in enumerate(case.problem.levels):
+        m = lvl.mesh
+        ui, uj = fem.pattern_from_elements(lvl.n_nodes, [m.cell_nodes[lvl.fluid_cells],
+                                                         m.cell_nodes[lvl.solid_cells],
+                                                         lvl.macro_nodes])
+        data = fem.union_layout(case.matrices[l], ui, uj)
+        S = fem.SplitBlockMatrix.from_union(lvl.n_nodes, ui, uj, data)
+        assert abs(S.to_csr() - case.matrices[l].to_csr()).max() == 0.0
+
+
 @pytest.mark.skipif(not rb.AVAILABLE, reason="reference not mounted")
 def test_live_reference_jacobian_2d_mini():
     """Entry-wise comparison with the reference's momentum_jacobian_data."""

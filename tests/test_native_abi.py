@@ -39,6 +39,14 @@ def test_abi_version_and_error_string():
         raise AssertionError("expected an argument error")
 
 
+def test_gmres_has_no_cpu_path():
+    import pytest
+    import scipy.sparse as sp
+    from paper_1904_02401_b200 import linsolve
+    with pytest.raises(TypeError):
+        linsolve.gmres(sp.identity(4), np.ones(4), preconditioner=None)
+
+
 def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     from paper_1904_02401_b200 import _lib
     monkeypatch.setattr(_lib, "_lib", None)
