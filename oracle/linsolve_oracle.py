@@ -199,18 +199,20 @@ class MgOracle:
     """V-cycle with Vanka smoothing and a sparse-LU coarse solve
     (linsolve.py:229-270)."""
 
-    def __init__(self, case, nu_pre=2, nu_post=2, omega=0.8, threads=1):
+    def __init__(self, case=None, nu_pre=2, nu_post=2, omega=0.8, threads=1, levels=None):
         self.nu_pre, self.nu_post = nu_pre, nu_post
-        self.nc = case.matrices[0].nc
-        self.A = [OracleOperator(m) for m in case.matrices]
-        self.P = case.prolongations
-        self.constrained = [lvl.momentum_dirichlet.reshape(-1) for lvl in case.problem.levels]
+        levels = levels if levels is not None else case.mg_levels()
+        mats = [lv["matrix"] for lv in levels]
+        self.nc = mats[0].nc
+        self.A = [OracleOperator(m) for m in mats]
+        self.P = [lv["P"] for lv in levels]
+        self.constrained = [np.asarray(lv["constrained"]).reshape(-1) for lv in levels]
         self.smoothers = [None]
         for l in range(1, len(self.A)):
-            sm = VankaOracle(case.patches[l], omega, threads)
-            sm.factorize(case.matrices[l])
+            sm = VankaOracle(levels[l]["patches"], omega, threads)
+            sm.factorize(mats[l])
             self.smoothers.append(sm)
-        self.coarse_lu = spla.splu(sp.csc_matrix(case.matrices[0].to_csr()))
+        self.coarse_lu = spla.splu(sp.csc_matrix(mats[0].to_csr()))
 
     def dot(self, b):
         return self.cycle(len(self.A) - 1, np.asarray(b, dtype=float))
@@ -232,6 +234,61 @@ class MgOracle:
         for _ in range(self.nu_post):
             x = sm.sweep(A, x, b)
         return x
+
+
+class OracleLinearStack:
+    """CPU counterpart of newton.LinearStack (reference newton.py:91-165) for
+    the Newton-loop parity runs: same assembly, oracle MG-GMRES solves."""
+
+    def __init__(self, problem, lin_cfg, threads=1):
+        from paper_1904_02401_b200 import mesh as mm, transfer
+        self.problem, self.cfg, self.threads = problem, lin_cfg, threads
+        levels = problem.levels
+        d = problem.dim
+        self.transfers = [None] + [transfer.prolongation(levels[l - 1].mesh, levels[l].mesh)
+                                   for l in range(1, len(levels))]
+        fs, ss = lin_cfg.patch_strategies(d)
+        self.mom_patches = [None] + [
+            mm.build_patches(levels[l].mesh, fs, n_comp=d + 1,
+                             per_subdomain={mm.FLUID: fs, mm.SOLID: ss})
+            for l in range(1, len(levels))]
+        self.ext_patches = [None] + [mm.build_patches(levels[l].mesh, mm.ONE_ELEMENT, n_comp=d)
+                                     for l in range(1, len(levels))]
+        self.mom_mg = None
+        self.ext_mg = None
+        self.last_rate = float("inf")
+
+    def build_momentum(self, U, U_prev, k, theta):
+        from paper_1904_02401_b200 import model
+        p = self.problem
+        levels = [{"matrix": model.momentum_jacobian(lvl, p.mats, p.flags, k, theta,
+                                                     p.restrict_state(U, l),
+                                                     p.restrict_state(U_prev, l)),
+                   "patches": self.mom_patches[l], "P": self.transfers[l],
+                   "constrained": lvl.momentum_dirichlet} for l, lvl in enumerate(p.levels)]
+        self.mom_mg = MgOracle(None, self.cfg.nu_pre, self.cfg.nu_post, self.cfg.omega,
+                               self.threads, levels=levels)
+
+    def solve_momentum(self, b):
+        return _solve(self.mom_mg, b, self.cfg.momentum_rel_tol, self.cfg.max_iter)
+
+    def solve_extension(self, b):
+        if self.ext_mg is None:
+            p = self.problem
+            levels = [{"matrix": p.extension_blocks(l)["bc"], "patches": self.ext_patches[l],
+                       "P": self.transfers[l], "constrained": lvl.ext_dirichlet}
+                      for l, lvl in enumerate(p.levels)]
+            self.ext_mg = MgOracle(None, self.cfg.nu_pre, self.cfg.nu_post, self.cfg.omega,
+                                   self.threads, levels=levels)
+        return _solve(self.ext_mg, b, self.cfg.extension_rel_tol, self.cfg.max_iter)
+
+
+def _solve(mg, b, rel_tol, max_iter):
+    from paper_1904_02401_b200.device import SolverError
+    try:
+        return gmres(mg.A[-1], b, mg, rel_tol=rel_tol, max_iter=max_iter)
+    except OracleSolverError as exc:
+        raise SolverError(str(exc), exc.stats) from exc
 
 
 def solve_case(case, wl, threads=1, mg=None):

@@ -73,15 +73,14 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
       const int64_t col = __ldcs(indices + blk);
       const double* v = data + blk * (NC * NC) + r * NC;
       const double* xv = x + col * NC;
-      if constexpr (NC == 4) {
-        const double2 v0 = __ldcs(reinterpret_cast<const double2*>(v));
-        const double2 v1 = __ldcs(reinterpret_cast<const double2*>(v) + 1);
-        const double2 x0 = __ldg(reinterpret_cast<const double2*>(xv));
-        const double2 x1 = __ldg(reinterpret_cast<const double2*>(xv) + 1);
-        acc = fma(v0.x, x0.x, acc);
-        acc = fma(v0.y, x0.y, acc);
-        acc = fma(v1.x, x1.x, acc);
-        acc = fma(v1.y, x1.y, acc);
+      if constexpr (NC % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < NC / 2; ++c) {
+          const double2 vv = __ldcs(reinterpret_cast<const double2*>(v) + c);
+          const double2 xx = __ldg(reinterpret_cast<const double2*>(xv) + c);
+          acc = fma(vv.x, xx.x, acc);
+          acc = fma(vv.y, xx.y, acc);
+        }
       } else {
 #pragma unroll
         for (int c = 0; c < NC; ++c) acc = fma(__ldcs(v + c), __ldg(xv + c), acc);
@@ -97,11 +96,10 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
     accp = warp_sum(accp);
   }
   double out[NC];
-  if constexpr (NC == 4) {
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 8);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-    // lanes 0..3 now hold rows 0..3
+  if constexpr (kWarp % NC == 0) {
+#pragma unroll
+    for (int o = NC; o < kWarp; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    // lanes 0..NC-1 now hold rows 0..NC-1
     if (lane < NC) {
       double v = acc + (lane == 0 ? accp : 0.0);
       const int64_t o = row * NC + lane;
@@ -587,6 +585,12 @@ void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y
   if (A.n_nodes == 0) return;
   if (A.nc == 4) spmv_dispatch<4>(A, x, b, y, mode, s);
   else if (A.nc == 3) spmv_dispatch<3>(A, x, b, y, mode, s);
+  else if (A.nc == 2) spmv_dispatch<2>(A, x, b, y, mode, s);
+}
+
+bool vanka_supported(int nc, int np) {
+  return (nc == 3 && (np == 27 || np == 75 || np == 81)) || (nc == 4 && np == 108) ||
+         (nc == 2 && np == 18);
 }
 
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,

@@ -32,6 +32,8 @@ struct DevPatchGroup {
   int64_t y_offset = 0;             // start of this group's rows in Y
 };
 
+// (nc, dofs per patch) combinations with compiled Vanka kernels
+bool vanka_supported(int nc, int np);
 // gather A_i = R_i A R_i^T and invert (Gauss-Jordan, partial pivoting);
 // singular patches set *status to 1 + patch index (first one wins)
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,

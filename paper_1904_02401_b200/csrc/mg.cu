@@ -670,6 +670,9 @@ int alefsi_mg_set_patches(alefsi_mg h, int32_t level, int32_t n_groups,
     auto g = std::make_unique<alefsi::Group>();
     g->npn = group_nodes_per_patch[gi];
     g->np = g->npn * nc;
+    if (!alefsi::vanka_supported(nc, g->np))
+      return fail(ALEFSI_ERR_ARG, "unsupported Vanka patch size " + std::to_string(g->np) +
+                                      " for nc=" + std::to_string(nc));
     g->ld = (g->np + 1) / 2 * 2;
     g->n_patches = group_n_patches[gi];
     g->y_offset = y_size;

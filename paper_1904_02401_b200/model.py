@@ -167,6 +167,190 @@ def _outflow_blocks(fq, U, mats, k, theta, d):
     return out
 
 
+def kinematics(grad_u):
+    """F = I + grad u, J, F^-1, E (reference model.py:65-75)."""
+    d = grad_u.shape[-1]
+    F = grad_u + np.eye(d)
+    J = np.linalg.det(F)
+    if np.any(J <= 0):
+        raise InvertedElementError(f"min det(F) = {np.min(J):g}")
+    return F, J, np.linalg.inv(F), 0.5 * (np.swapaxes(F, -1, -2) @ F - np.eye(d))
+
+
+def _svk(F, E, mats):
+    """First Piola stress F Sigma of St. Venant-Kirchhoff (model.py:101-106)."""
+    d = F.shape[-1]
+    tr = np.trace(E, axis1=-2, axis2=-1)
+    return F @ (2.0 * mats.mu_s * E + mats.lam_s * tr[..., None, None] * np.eye(d))
+
+
+def deformation_update(U, U_prev, k, theta, nodes):
+    """u_n = u_{n-1} + k theta v_n + k (1-theta) v_{n-1} on nodes (model.py:109-114)."""
+    d = (U.shape[1] - 1) // 2
+    U[nodes, 1 + d:] = (U_prev[nodes, 1 + d:] + k * theta * U[nodes, 1:1 + d]
+                        + k * (1.0 - theta) * U_prev[nodes, 1:1 + d])
+
+
+def _test(wdet, N, G, val, grad):
+    """sum_q w (N_b val_i + G_b . grad_i) -> (c, b, i) (model.py:147-154)."""
+    out = 0.0
+    if val is not None:
+        out = out + np.einsum("cq,qb,cqi->cbi", wdet, N, val, optimize=True)
+    if grad is not None:
+        out = out + np.einsum("cq,cqbj,cqij->cbi", wdet, G, grad, optimize=True)
+    return out
+
+
+def _qfields(lvl, cells, U):
+    d = lvl.dim
+    Uc = U[lvl.mesh.cell_nodes[cells]]
+    N = lvl.table.N
+    p = N @ Uc[:, :, 0].T
+    v, u, gv, gu = _fields(lvl.G[cells], N, Uc, d)
+    return p.T, v, u, gv, gu
+
+
+def outflow_correction(lvl, mats, U, X, scale=1.0):
+    """Do-nothing correction -(mu J F^-T grad(v)^T F^-T n, phi) on the outflow
+    facets (reference model.py:191-205)."""
+    fq = lvl.outflow
+    if fq is None:
+        return
+    d = lvl.dim
+    gv = fq.eval_grad(U[:, 1:1 + d])
+    gu = fq.eval_grad(U[:, 1 + d:])
+    _, J, Fi = _fluid_kin(gu)
+    FiT = np.swapaxes(Fi, -1, -2)
+    t = np.einsum("cqij,cqj->cqi", FiT @ np.swapaxes(gv, -1, -2) @ FiT, fq.normal)
+    local = np.einsum("cq,cqb,cqi->cbi", fq.dS, fq.N, -scale * mats.mu_f * J[..., None] * t)
+    np.add.at(X, fq.conn, local)
+
+
+def explicit_forces(lvl, mats, flags, U_prev):
+    """A_F + A_S of the previous state (reference model.py:159-188)."""
+    d = lvl.dim
+    X = np.zeros((lvl.n_nodes, d))
+    f = np.asarray(mats.body_force, dtype=float)
+    cells = lvl.fluid_cells
+    if len(cells):
+        _, v, _, gv, gu = _qfields(lvl, cells, U_prev)
+        _, J, Fi = _fluid_kin(gu)
+        gvFi = gv @ Fi
+        conv = mats.rho_f * J[..., None] * np.einsum("cqij,cqj->cqi", gvFi, v)
+        conv = conv - mats.rho_f * J[..., None] * f
+        visc = mats.mu_f * J[..., None, None] * ((gvFi + np.swapaxes(gvFi, -1, -2))
+                                                 @ np.swapaxes(Fi, -1, -2))
+        np.add.at(X, lvl.mesh.cell_nodes[cells],
+                  _test(lvl.wdet[cells], lvl.table.N, lvl.G[cells], conv, visc))
+    cells = lvl.solid_cells
+    if len(cells):
+        _, v, _, _, gu = _qfields(lvl, cells, U_prev)
+        F, _, _, E = kinematics(gu)
+        sval = -mats.rho_s * np.broadcast_to(f, v.shape)
+        np.add.at(X, lvl.mesh.cell_nodes[cells],
+                  _test(lvl.wdet[cells], lvl.table.N, lvl.G[cells], sval, _svk(F, E, mats)))
+    outflow_correction(lvl, mats, U_prev, X)
+    return X
+
+
+def theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit=None):
+    """Residual of one theta step with constrained rows zeroed
+    (reference model.py:208-292).  Returns (R, explicit)."""
+    with fem.single_blas():
+        return _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit)
+
+
+def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
+    d = lvl.dim
+    n = lvl.n_nodes
+    if explicit is None:
+        explicit = explicit_forces(lvl, mats, flags, U_prev)
+    R = np.zeros((n, 1 + 2 * d))
+    f = np.asarray(mats.body_force, dtype=float)
+    N = lvl.table.N
+    cells = lvl.fluid_cells
+    if len(cells):
+        wdet, G = lvl.wdet[cells], lvl.G[cells]
+        p, v, u, gv, gu = _qfields(lvl, cells, U)
+        _, vp, up, gvp, gup = _qfields(lvl, cells, U_prev)
+        F, J, Fi = _fluid_kin(gu)
+        Fp, Jp, _ = _fluid_kin(gup)
+        Jbar = 0.5 * (J + Jp)
+        w = np.einsum("cqij,cqj->cqi", np.linalg.inv(0.5 * (F + Fp)), u - up)
+        gvFi = gv @ Fi
+        mom_val = (mats.rho_f * Jbar[..., None] * (v - vp)
+                   - mats.rho_f * Jbar[..., None] * np.einsum("cqij,cqj->cqi", 0.5 * (gv + gvp), w)
+                   + k * theta * mats.rho_f * J[..., None]
+                   * (np.einsum("cqij,cqj->cqi", gvFi, v) - f))
+        FiT = np.swapaxes(Fi, -1, -2)
+        mom_grad = (k * theta * mats.mu_f * J[..., None, None]
+                    * (gvFi + np.swapaxes(gvFi, -1, -2)) @ FiT
+                    - k * (J * p)[..., None, None] * FiT)
+        div_val = k * J * np.einsum("cqij,cqji->cq", gv, Fi)
+        if flags.extension_model == "harmonic":
+            ext_grad = k * gu
+        else:
+            eps = 0.5 * (gu + np.swapaxes(gu, -1, -2))
+            tr = np.einsum("cqii->cq", eps)
+            ext_grad = k * (2.0 * flags.ext_mu * eps + flags.ext_lam * tr[..., None, None] * np.eye(d))
+            if flags.ext_volume_scaling:
+                ext_grad = ext_grad * lvl.inv_cell_volume[cells][:, None, None, None]
+        local = np.zeros((len(cells), N.shape[1], 1 + 2 * d))
+        local[:, :, 0] = np.einsum("cq,qb,cq->cb", wdet, N, div_val)
+        local[:, :, 1:1 + d] = _test(wdet, N, G, mom_val, mom_grad)
+        local[:, :, 1 + d:] = _test(wdet, N, G, None, ext_grad)
+        np.add.at(R, lvl.mesh.cell_nodes[cells], local)
+    cells = lvl.solid_cells
+    if len(cells):
+        wdet, G = lvl.wdet[cells], lvl.G[cells]
+        _, v, _, gv, _ = _qfields(lvl, cells, U)
+        _, vp, _, gvp, gup = _qfields(lvl, cells, U_prev)
+        F, _, _, E = kinematics(gup + k * theta * gv + k * (1.0 - theta) * gvp)
+        sval = mats.rho_s * (v - vp) - k * theta * mats.rho_s * f
+        local = np.zeros((len(cells), N.shape[1], 1 + 2 * d))
+        local[:, :, 1:1 + d] = _test(wdet, N, G, sval, k * theta * _svk(F, E, mats))
+        np.add.at(R, lvl.mesh.cell_nodes[cells], local)
+    R[:, 1:1 + d] += k * (1.0 - theta) * explicit
+    Xc = np.zeros((n, d))
+    outflow_correction(lvl, mats, U, Xc, scale=k * theta)
+    R[:, 1:1 + d] += Xc
+    R[:, 0] += k * (lvl.lps_csr() @ U[:, 0])
+    deficit = (U[:, 1 + d:] - U_prev[:, 1 + d:] - k * theta * U[:, 1:1 + d]
+               - k * (1.0 - theta) * U_prev[:, 1:1 + d])
+    rel = lvl.solid_mass_csr() @ deficit
+    R[lvl.relation_nodes, 1 + d:] = rel[lvl.relation_nodes]
+    R[lvl.residual_zero_mask] = 0.0
+    return R, explicit
+
+
+def extension_operator(lvl, flags):
+    """State-independent mesh-extension operator on the fluid cells
+    (reference model.py:442-461), split layout with nc = d."""
+    d = lvl.dim
+    import dataclasses
+    # cell-stencil blocks only: the extension has no LPS macro couplings
+    p = dataclasses.replace(lvl.pattern, pp_indptr=np.zeros(lvl.n_nodes + 1, dtype=np.int64),
+                            pp_indices=np.zeros(0, dtype=np.int32))
+    A = fem.SplitBlockMatrix(p, np.zeros((p.nnzb, d, d)), np.zeros(0))
+    cells = lvl.fluid_cells
+    if len(cells) == 0:
+        return A
+    with fem.single_blas():
+        wdet, G = lvl.wdet[cells], lvl.G[cells]
+        if flags.extension_model == "harmonic":
+            gg = np.einsum("cq,cqam,cqbm->cba", wdet, G, G, optimize=True)
+            local = gg[..., None, None] * np.eye(d)
+        else:
+            scale = lvl.inv_cell_volume[cells] if flags.ext_volume_scaling else np.ones(len(cells))
+            w = wdet * scale[:, None]
+            gg = np.einsum("cq,cqam,cqbm->cba", w, G, G, optimize=True)
+            local = flags.ext_mu * gg[..., None, None] * np.eye(d)
+            local = local + flags.ext_mu * np.einsum("cq,cqai,cqbj->cbaij", w, G, G, optimize=True)
+            local = local + flags.ext_lam * np.einsum("cq,cqaj,cqbi->cbaij", w, G, G, optimize=True)
+        fem.scatter_blocks(p.indptr, p.indices, A.data, lvl.mesh.cell_nodes[cells], local)
+    return A
+
+
 def momentum_jacobian(lvl, mats, flags, k, theta, U, U_prev, chunk=2048):
     """Reduced (p, v) Jacobian on one level in the split block layout."""
     with fem.single_blas():

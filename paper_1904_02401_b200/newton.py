@@ -9,7 +9,10 @@ whose ``solve_momentum`` runs GMRES + V-cycle — here on the device.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
 
 from . import linsolve, model
 from .mesh import MULTI_ELEMENT, ONE_ELEMENT
@@ -72,3 +75,206 @@ class LinearStack:
         """GMRES + V-cycle on the finest momentum system (newton.py:153-157)."""
         return linsolve.gmres(self.mom_mg.levels[-1].matrix, b, self.mom_mg,
                               rel_tol=self.cfg.momentum_rel_tol, max_iter=self.cfg.max_iter)
+
+    # extension stack: state independent, assembled and factorised once
+    def _build_extension(self):
+        p = self.problem
+        d = p.dim
+        levels = []
+        for l, lvl in enumerate(p.levels):
+            sm = None
+            if l > 0:
+                ps, col = linsolve.build_extension_patches(lvl.mesh, d, ONE_ELEMENT)
+                sm = linsolve.VankaSmoother(ps, col, self.cfg.omega)
+            levels.append(linsolve.MgLevel(matrix=p.extension_blocks(l)["bc"], smoother=sm,
+                                           P=self.transfers[l],
+                                           constrained=lvl.ext_dirichlet.reshape(-1)))
+        self.ext_mg = linsolve.MgSolver(levels, self.cfg.nu_pre, self.cfg.nu_post,
+                                        use_graph=self.cfg.use_graph)
+
+    def solve_extension(self, b):
+        """GMRES + V-cycle on the mesh-extension system (newton.py:159-165)."""
+        if getattr(self, "ext_mg", None) is None:
+            self._build_extension()
+        return linsolve.gmres(self.ext_mg.levels[-1].matrix, b, self.ext_mg,
+                              rel_tol=self.cfg.extension_rel_tol, max_iter=self.cfg.max_iter)
+
+
+# ---------------------------------------------------------------------------------
+# Approximated Newton iteration and time loop (reference newton.py:27-365)
+# ---------------------------------------------------------------------------------
+
+class StepFailure(Exception):
+    def __init__(self, message, stats=None):
+        super().__init__(message)
+        self.stats = stats
+
+
+@dataclass
+class NewtonConfig:
+    rel_tol: float = 1e-8
+    abs_tol: float = 1e-8
+    max_steps: int = 30
+    gamma: float = 0.05
+    max_halvings: int = 4
+
+
+@dataclass
+class TimeLoopConfig:
+    k: float = 0.004
+    theta_rule: str = "shifted_cn"
+    t_start: float = 0.0
+    t_end: float = 1.0
+
+
+def theta_for(rule, k):
+    if rule == "shifted_cn":
+        return 0.5 + 2.0 * k
+    if rule == "backward_euler":
+        return 1.0
+    return float(rule)
+
+
+@dataclass
+class NewtonStats:
+    steps: int = 0
+    assemblies: int = 0
+    rates: list = field(default_factory=list)
+    momentum_iters: list = field(default_factory=list)
+    extension_iters: list = field(default_factory=list)
+    residuals: list = field(default_factory=list)
+    assemble_time: float = 0.0
+    solve_time: float = 0.0
+    residual_time: float = 0.0
+    converged: bool = False
+
+
+def solve_reduced_linear(problem, stack, R, U, U_prev, k, theta):
+    """Three-stage exact solve of the reduced system (reference
+    newton.py:168-201): momentum (device MG-GMRES), deformation update (vector
+    addition), mesh extension (device MG-GMRES)."""
+    lvl = problem.fine
+    d = lvl.dim
+    n = lvl.n_nodes
+    x, mom_stats = stack.solve_momentum(-R[:, :d + 1].reshape(-1))
+    dpv = np.asarray(x).reshape(n, d + 1)
+    rel = lvl.relation_nodes
+    deficit = (U[:, 1 + d:] - U_prev[:, 1 + d:] - k * theta * U[:, 1:1 + d]
+               - k * (1.0 - theta) * U_prev[:, 1:1 + d])
+    du = np.zeros((n, d))
+    du[rel] = k * theta * dpv[rel, 1:] - deficit[rel]
+    blocks = problem.extension_blocks(len(problem.levels) - 1)
+    g = np.zeros((n, d))
+    g[lvl.interface_nodes] = du[lvl.interface_nodes]
+    rhs = -R[:, 1 + d:] / k - (blocks["raw_csr"] @ g.reshape(-1)).reshape(n, d)
+    rhs[lvl.ext_dirichlet] = 0.0
+    z, ext_stats = stack.solve_extension(rhs.reshape(-1))
+    W = np.zeros_like(U)
+    W[:, :d + 1] = dpv
+    W[:, 1 + d:] = np.asarray(z).reshape(n, d)
+    W[lvl.interface_nodes, 1 + d:] = du[lvl.interface_nodes]
+    W[rel, 1 + d:] = du[rel]
+    W[lvl.u_dirichlet_nodes, 1 + d:] = 0.0
+    return W, mom_stats, ext_stats
+
+
+def line_search(residual_of, U, W, res_norm, max_halvings=4):
+    """Backtracking by halving on the residual sup-norm (newton.py:204-216)."""
+    omega = 1.0
+    for _ in range(max_halvings + 1):
+        payload, res_try = residual_of(U + omega * W)
+        if res_try <= res_norm:
+            return omega, payload, res_try
+        omega *= 0.5
+    raise StepFailure("line search exhausted: residual would increase")
+
+
+def newton_solve(problem, stack, U_guess, U_prev, k, theta, cfg: NewtonConfig):
+    """Approximated Newton iteration for one time step (newton.py:219-273):
+    reassemble the momentum Jacobian only when the last rate exceeds gamma."""
+    lvl = problem.fine
+    stats = NewtonStats()
+    cache = [None]
+
+    def residual_of(Ut):
+        Ut = Ut.copy()
+        model.deformation_update(Ut, U_prev, k, theta, lvl.relation_nodes)
+        t0 = time.perf_counter()
+        R, cache[0] = model.theta_residual(lvl, problem.mats, problem.flags, k, theta, Ut,
+                                           U_prev, cache[0])
+        stats.residual_time += time.perf_counter() - t0
+        return (Ut, R), float(np.abs(R).max())
+
+    (U, R), res = residual_of(U_guess)
+    stats.residuals.append(res)
+    tol = max(cfg.abs_tol, cfg.rel_tol * res)
+    while res > tol:
+        if stats.steps >= cfg.max_steps:
+            raise StepFailure(f"Newton did not converge in {cfg.max_steps} steps "
+                              f"(residual {res:.3e})", stats)
+        if stack.mom_mg is None or stack.last_rate > cfg.gamma:
+            t0 = time.perf_counter()
+            stack.build_momentum(U, U_prev, k, theta)
+            stats.assemble_time += time.perf_counter() - t0
+            stats.assemblies += 1
+        t0 = time.perf_counter()
+        try:
+            W, ms, es = solve_reduced_linear(problem, stack, R, U, U_prev, k, theta)
+        except linsolve.SolverError as exc:
+            raise StepFailure(f"linear solve failed: {exc}", stats) from exc
+        stats.solve_time += time.perf_counter() - t0
+        stats.momentum_iters.append(ms.iterations)
+        stats.extension_iters.append(es.iterations)
+        try:
+            _, (U, R), res_new = line_search(residual_of, U, W, res, cfg.max_halvings)
+        except StepFailure as exc:
+            exc.stats = stats
+            raise
+        rate = res_new / res if res > 0 else 0.0
+        stack.last_rate = rate
+        stats.rates.append(rate)
+        stats.residuals.append(res_new)
+        stats.steps += 1
+        res = res_new
+    stats.converged = True
+    return U, stats
+
+
+def run_time_loop(problem, tl: TimeLoopConfig, newton_cfg: NewtonConfig, stack,
+                  U0=None, on_step=None):
+    """Advance from t_start to t_end; a failing step is retried once as two
+    half steps (reference newton.py:303-364).  Returns (U, per-step stats)."""
+    if U0 is None:
+        U0 = problem.zero_state()
+        problem.impose_boundary_values(U0, tl.t_start)
+    t = tl.t_start
+    U_prev = U0
+    all_stats = []
+    while t < tl.t_end - 1e-12:
+        k = min(tl.k, tl.t_end - t)
+        t0 = time.perf_counter()
+        U_n, sl = _advance(problem, stack, U_prev, t, k, tl, newton_cfg, True)
+        wall = time.perf_counter() - t0
+        t = t + k
+        if on_step is not None:
+            on_step(t, U_n, U_prev, k, theta_for(tl.theta_rule, k), sl, wall)
+        all_stats.append((t, wall, sl))
+        U_prev = U_n
+    return U_prev, all_stats
+
+
+def _advance(problem, stack, U_prev, t, k, tl, cfg, allow_halving):
+    theta = theta_for(tl.theta_rule, k)
+    guess = U_prev.copy()
+    problem.impose_boundary_values(guess, t + k)
+    try:
+        U_n, stats = newton_solve(problem, stack, guess, U_prev, k, theta, cfg)
+        return U_n, [stats]
+    except StepFailure:
+        stack.last_rate = float("inf")
+        if not allow_halving:
+            raise
+        half = k / 2.0
+        U_mid, s1 = _advance(problem, stack, U_prev, t, half, tl, cfg, False)
+        U_n, s2 = _advance(problem, stack, U_mid, t + half, half, tl, cfg, False)
+        return U_n, s1 + s2

@@ -127,6 +127,90 @@ CONFIGS = {
 }
 
 
+# -- BASELINE config 4: implicit time stepping with the approximated Newton ----
+
+@dataclass
+class TimeStepping:
+    """10 implicit steps from rest driven by a parabolic inflow of peak 1.0,
+    do-nothing outflow, no-slip walls, harmonic mesh extension (config 4)."""
+
+    base: Workload
+    n_steps: int = 10
+    momentum_rel_tol: float = 1e-4       # reference LinearConfig default
+    extension_rel_tol: float = 1e-8
+    newton_rel_tol: float = 1e-8
+    newton_abs_tol: float = 1e-8
+    gamma: float = 0.05
+
+    def inflow(self, points, t):
+        L = self.base.lengths
+        out = np.zeros_like(points)
+        prof = np.ones(len(points))
+        for i in range(1, points.shape[1]):
+            y = points[:, i] / L[i]
+            prof = prof * 4.0 * y * (1.0 - y)
+        out[:, 0] = prof
+        return out
+
+    def flags(self):
+        return FsiFlags(lps_dt=self.base.dt, extension_model="harmonic")
+
+    def problem(self):
+        return FsiProblem(self.base.hierarchy(), self.base.materials(), self.flags(),
+                          inflow_fn=self.inflow)
+
+    def configs(self):
+        from . import newton
+        fs, ss = self.base.patch_strategies()
+        lin = newton.LinearConfig(momentum_rel_tol=self.momentum_rel_tol,
+                                  extension_rel_tol=self.extension_rel_tol,
+                                  max_iter=self.base.max_iter, nu_pre=self.base.nu_pre,
+                                  nu_post=self.base.nu_post, omega=self.base.omega,
+                                  fluid_patches=fs, solid_patches=ss)
+        nt = newton.NewtonConfig(rel_tol=self.newton_rel_tol, abs_tol=self.newton_abs_tol,
+                                 gamma=self.gamma)
+        tl = newton.TimeLoopConfig(k=self.base.dt, theta_rule="shifted_cn", t_start=0.0,
+                                   t_end=self.n_steps * self.base.dt)
+        return lin, nt, tl
+
+
+TIMESTEPPING = {
+    "3d_timestep": TimeStepping(CONFIGS["3d_small"]),          # BASELINE config 4
+    "2d_timestep_mini": TimeStepping(CONFIGS["2d_mini"], n_steps=3),
+    "3d_timestep_tiny": TimeStepping(CONFIGS["3d_tiny"], n_steps=2),
+}
+
+
+def run_timestepping(ts: TimeStepping, stack_factory, on_step=None, n_steps=None):
+    """Run the time loop with a linear stack from ``stack_factory(problem,
+    lin_cfg)`` (device LinearStack or the CPU oracle's).  Returns
+    (U_final, records) with per-step Newton/GMRES statistics."""
+    from . import newton
+    problem = ts.problem()
+    lin, nt, tl = ts.configs()
+    if n_steps is not None:
+        tl.t_end = n_steps * ts.base.dt
+    stack = stack_factory(problem, lin)
+    records = []
+
+    def cb(t, U, U_prev, k, theta, stats_list, wall):
+        rec = {"t": t, "wall_s": wall,
+               "newton_steps": [s.steps for s in stats_list],
+               "assemblies": [s.assemblies for s in stats_list],
+               "momentum_iters": [list(s.momentum_iters) for s in stats_list],
+               "extension_iters": [list(s.extension_iters) for s in stats_list],
+               "residuals": [list(s.residuals) for s in stats_list],
+               "assemble_s": sum(s.assemble_time for s in stats_list),
+               "solve_s": sum(s.solve_time for s in stats_list),
+               "residual_s": sum(s.residual_time for s in stats_list)}
+        records.append(rec)
+        if on_step is not None:
+            on_step(rec, U)
+
+    U, _ = newton.run_time_loop(problem, tl, nt, stack, on_step=cb)
+    return U, records
+
+
 def sine_field(rng, X, lengths, ncomp, n_modes=8):
     """Sum of n_modes sine modes vanishing on the box boundary."""
     out = np.zeros((len(X), ncomp))

@@ -85,9 +85,26 @@ def run(name, solve_only=False):
     print(name, "iterations", st.iterations, "setup %.1fs solve %.1fs" % (t1 - t0, t2 - t1))
 
 
+def run_timestep(name, n_steps=None):
+    """The reference's run_time_loop on a TimeStepping workload (config 4
+    family): per-step Newton/GMRES statistics and the final state."""
+    ts = W.TIMESTEPPING[name]
+    t0 = time.perf_counter()
+    U, records = rb.ref_timestepping(ts, n_steps)
+    out = {"workload": name, "n_steps": len(records), "records": records,
+           "U_checksums": vector_checksums(U.reshape(-1)), "ref_wall_s": time.perf_counter() - t0}
+    with open(os.path.join(HERE, f"{name}.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print(name, [r["newton_steps"] for r in records], "%.1fs" % out["ref_wall_s"])
+
+
 if __name__ == "__main__":
     args = sys.argv[1:]
     solve_only = "--solve-only" in args
     for a in args:
-        if not a.startswith("--"):
+        if a.startswith("--"):
+            continue
+        if a in W.TIMESTEPPING:
+            run_timestep(a)
+        else:
             run(a, solve_only)

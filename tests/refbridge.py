@@ -43,6 +43,38 @@ def ref_problem(wl):
     return a.problem.FsiProblem(h, mats, flags)
 
 
+def ref_timestepping(ts, n_steps=None):
+    """The reference's own run_time_loop (newton.py:303-343) on a
+    TimeStepping workload; returns (U, per-step records)."""
+    a = ref()
+    wl = ts.base
+    prob = ref_problem(wl)
+    prob.flags.extension_model = "harmonic"
+    prob.inflow_fn = ts.inflow
+    lin, nt, tl = ts.configs()
+    if n_steps is not None:
+        tl.t_end = n_steps * wl.dt
+    rlin = a.newton.LinearConfig(momentum_rel_tol=lin.momentum_rel_tol,
+                                 extension_rel_tol=lin.extension_rel_tol, max_iter=lin.max_iter,
+                                 nu_pre=lin.nu_pre, nu_post=lin.nu_post, omega=lin.omega,
+                                 fluid_patches=lin.fluid_patches, solid_patches=lin.solid_patches)
+    rnt = a.newton.NewtonConfig(rel_tol=nt.rel_tol, abs_tol=nt.abs_tol, gamma=nt.gamma,
+                                max_steps=nt.max_steps, max_halvings=nt.max_halvings)
+    rtl = a.newton.TimeLoopConfig(k=tl.k, theta_rule=tl.theta_rule, t_start=tl.t_start,
+                                  t_end=tl.t_end)
+    records = []
+
+    def cb(t, U, U_prev, k, theta, stats_list):
+        records.append({"t": t,
+                        "newton_steps": [s.steps for s in stats_list],
+                        "assemblies": [s.assemblies for s in stats_list],
+                        "momentum_iters": [list(s.momentum_iters) for s in stats_list],
+                        "extension_iters": [list(s.extension_iters) for s in stats_list],
+                        "residuals": [[float(r) for r in s.residuals] for s in stats_list]})
+    state, _ = a.newton.run_time_loop(prob, rtl, rnt, rlin, on_step=cb)
+    return state.U, records
+
+
 def ref_stack(wl, prob, U, Up):
     a = ref()
     fp, spt = wl.patch_strategies()
