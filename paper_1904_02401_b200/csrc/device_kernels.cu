@@ -180,27 +180,29 @@ __global__ void vanka_gather_kernel(int64_t ndof, int nc, const int64_t* __restr
   x[t] = __dadd_rn(base, __dmul_rn(omega, acc));
 }
 
-// Gather A_p = R_p A R_p^T into shared memory and invert it in place by
-// Gauss-Jordan elimination with partial (row) pivoting; columns are
-// unscrambled at the end.  One CTA per patch.
-template <int NP, int NC>
-__global__ void __launch_bounds__(256) vanka_factorize_kernel(DevMatrix A, int64_t n_patches,
-                                                              const int32_t* __restrict__ nodes,
-                                                              double* __restrict__ inv, int ld,
-                                                              int64_t* status) {
-  constexpr int NPN = NP / NC;
-  extern __shared__ double smem[];
-  double* M = smem;                                   // NP*NP row-major
-  double* colk = M + NP * NP;                         // NP
-  int64_t* slotB = reinterpret_cast<int64_t*>(colk + NP);
-  int64_t* slotP = slotB + NPN * NPN;
-  int* perm = reinterpret_cast<int*>(slotP + NPN * NPN);
+// Register-tiled Gauss-Jordan inversion with implicit partial pivoting.
+// A TY x TX thread grid owns the patch matrix in registers (thread (ty,tx)
+// holds rows ty+TY*i, columns tx+TX*j); per pivot step only the pivot column
+// and the scaled pivot row go through shared memory.  Rows are never
+// swapped: step k pivots on the largest unused row p_k of column k (the
+// pivot LAPACK's getrf would choose), and at the end
+//     inv[q(r)][p_c] = R[r][c],   q = p^{-1},
+// which is written directly in the column-major (ld) layout.
+template <int NP, int NC, int TY, int TX>
+__global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
+    DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
+    int ld, int64_t* status) {
+  constexpr int NPN = NP / NC, RT = (NP + TY - 1) / TY, CT = (NP + TX - 1) / TX, NT = TY * TX;
+  static_assert(NT >= 32, "need at least one full warp");
+  __shared__ int64_t slotB[NPN * NPN], slotP[NPN * NPN];
+  __shared__ double colk[NP], prow[NP];
+  __shared__ int used[NP], prow_of_step[NP], step_of_row[NP];
   __shared__ int piv_row;
-  const int tid = threadIdx.x, bd = blockDim.x;
+  const int tid = threadIdx.x, ty = tid / TX, tx = tid - (tid / TX) * TX;
   const int64_t p = blockIdx.x;
   if (p >= n_patches) return;
   const int32_t* pn = nodes + p * NPN;
-  for (int t = tid; t < NPN * NPN; t += bd) {
+  for (int t = tid; t < NPN * NPN; t += NT) {
     const int a = t / NPN, b = t - a * NPN;
     const int64_t ra = pn[a];
     const int32_t cb = pn[b];
@@ -222,24 +224,45 @@ __global__ void __launch_bounds__(256) vanka_factorize_kernel(DevMatrix A, int64
     }
     slotP[t] = sp;
   }
+  for (int i = tid; i < NP; i += NT) used[i] = 0;
   __syncthreads();
-  for (int e = tid; e < NP * NP; e += bd) {
-    const int i = e / NP, j = e - i * NP;
-    const int a = i / NC, ci = i - a * NC, b = j / NC, cj = j - b * NC;
-    const int t = a * NPN + b;
-    double v = 0.0;
-    if (slotB[t] >= 0) v = A.data[slotB[t] * (NC * NC) + ci * NC + cj];
-    else if (ci == 0 && cj == 0 && slotP[t] >= 0) v = A.pp_data[slotP[t]];
-    M[e] = v;
-  }
-  __syncthreads();
+  double M[RT][CT];
+#pragma unroll
+  for (int i = 0; i < RT; ++i)
+#pragma unroll
+    for (int j = 0; j < CT; ++j) {
+      const int r = ty + TY * i, c = tx + TX * j;
+      double v = 0.0;
+      if (r < NP && c < NP) {
+        const int a = r / NC, ci = r - a * NC, b = c / NC, cj = c - b * NC;
+        const int t = a * NPN + b;
+        if (slotB[t] >= 0) v = A.data[slotB[t] * (NC * NC) + ci * NC + cj];
+        else if (ci == 0 && cj == 0 && slotP[t] >= 0) v = A.pp_data[slotP[t]];
+      }
+      M[i][j] = v;
+    }
   for (int k = 0; k < NP; ++k) {
+    // 1. owners of column k publish it
+    if (tx == k % TX) {
+      const int jk = k / TX;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = ty + TY * i;
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < CT; ++j)
+          if (j == jk) v = M[i][j];
+        if (r < NP) colk[r] = v;
+      }
+    }
+    __syncthreads();
+    // 2. pivot: largest |.| among unused rows, lowest index on ties
     if (tid < 32) {
       double best = -1.0;
-      int bi = k;
-      for (int i = k + tid; i < NP; i += 32) {
-        const double v = fabs(M[i * NP + k]);
-        if (v > best) { best = v; bi = i; }
+      int bi = NP;
+      for (int r = tid; r < NP; r += 32) {
+        const double v = used[r] ? -1.0 : fabs(colk[r]);
+        if (v > best) { best = v; bi = r; }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -247,51 +270,64 @@ __global__ void __launch_bounds__(256) vanka_factorize_kernel(DevMatrix A, int64
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
-      if (tid == 0) { piv_row = bi; perm[k] = bi; }
+      if (tid == 0) {
+        piv_row = bi;
+        used[bi] = 1;
+        prow_of_step[k] = bi;
+        step_of_row[bi] = k;
+      }
     }
     __syncthreads();
     const int pr = piv_row;
-    if (pr != k)
-      for (int j = tid; j < NP; j += bd) {
-        const double tmp = M[k * NP + j];
-        M[k * NP + j] = M[pr * NP + j];
-        M[pr * NP + j] = tmp;
-      }
-    __syncthreads();
-    const double piv = M[k * NP + k];
+    const double piv = colk[pr];
     if (piv == 0.0) {
       if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
                               (unsigned long long)(p + 1));
       return;
     }
     const double rp = 1.0 / piv;
-    for (int i = tid; i < NP; i += bd) colk[i] = M[i * NP + k];
+    // 3. owners of the pivot row scale it and publish it
+    if (ty == pr % TY) {
+      const int ip = pr / TY;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        if (i != ip) continue;
+#pragma unroll
+        for (int j = 0; j < CT; ++j) {
+          const int c = tx + TX * j;
+          const double v = (c == k) ? rp : M[i][j] * rp;
+          M[i][j] = v;
+          if (c < NP) prow[c] = v;
+        }
+      }
+    }
     __syncthreads();
-    for (int j = tid; j < NP; j += bd) M[k * NP + j] = (j == k) ? rp : M[k * NP + j] * rp;
-    __syncthreads();
-    for (int e = tid; e < NP * NP; e += bd) {
-      const int i = e / NP, j = e - i * NP;
-      if (i == k) continue;
-      const double f = colk[i];
-      M[e] = (j == k) ? -f * rp : M[e] - f * M[k * NP + j];
+    // 4. eliminate column k from every other row
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      const int r = ty + TY * i;
+      if (r == pr || r >= NP) continue;
+      const double f = colk[r];
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        const int c = tx + TX * j;
+        if (c >= NP) continue;
+        M[i][j] = (c == k) ? -f * rp : fma(-f, prow[c], M[i][j]);
+      }
     }
     __syncthreads();
   }
-  for (int k = NP - 1; k >= 0; --k) {
-    const int pr = perm[k];
-    if (pr != k)
-      for (int i = tid; i < NP; i += bd) {
-        const double tmp = M[i * NP + k];
-        M[i * NP + k] = M[i * NP + pr];
-        M[i * NP + pr] = tmp;
-      }
-    __syncthreads();
-  }
   double* out = inv + p * (int64_t)NP * ld;
-  for (int e = tid; e < NP * ld; e += bd) {
-    const int j = e / ld, i = e - j * ld;
-    out[e] = i < NP ? M[i * NP + j] : 0.0;
-  }
+#pragma unroll
+  for (int i = 0; i < RT; ++i)
+#pragma unroll
+    for (int j = 0; j < CT; ++j) {
+      const int r = ty + TY * i, c = tx + TX * j;
+      if (r < NP && c < NP) out[(int64_t)prow_of_step[c] * ld + step_of_row[r]] = M[i][j];
+    }
+  if (ld > NP)
+    for (int col = tid; col < NP; col += NT)
+      for (int r = NP; r < ld; ++r) out[(int64_t)col * ld + r] = 0.0;
 }
 
 // --------------------------------------------------------------------------
@@ -566,16 +602,11 @@ void apply_dispatch(const DevPatchGroup& g, const double* d, double* Y, cudaStre
                                                        Y + g.y_offset);
 }
 
-template <int NP, int NC>
+template <int NP, int NC, int TY, int TX>
 void factorize_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                         cudaStream_t s) {
-  constexpr int NPN = NP / NC;
-  const size_t smem = sizeof(double) * (NP * NP + NP) + sizeof(int64_t) * 2 * NPN * NPN +
-                      sizeof(int) * NP;
-  cudaFuncSetAttribute(vanka_factorize_kernel<NP, NC>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  vanka_factorize_kernel<NP, NC><<<(unsigned)g.n_patches, 256, smem, s>>>(A, g.n_patches, g.nodes,
-                                                                         g.inv, g.ld, status);
+  vanka_factorize_rt_kernel<NP, NC, TY, TX><<<(unsigned)g.n_patches, TY * TX, 0, s>>>(
+      A, g.n_patches, g.nodes, g.inv, g.ld, status);
 }
 
 }  // namespace
@@ -596,11 +627,11 @@ bool vanka_supported(int nc, int np) {
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                             cudaStream_t s) {
   if (g.n_patches == 0) return;
-  if (A.nc == 3 && g.np == 27) factorize_dispatch<27, 3>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 75) factorize_dispatch<75, 3>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108) factorize_dispatch<108, 4>(A, g, status, s);
-  else if (A.nc == 2 && g.np == 18) factorize_dispatch<18, 2>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 81) factorize_dispatch<81, 3>(A, g, status, s);
+  if (A.nc == 3 && g.np == 27) factorize_dispatch<27, 3, 9, 9>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 75) factorize_dispatch<75, 3, 15, 15>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108) factorize_dispatch<108, 4, 27, 12>(A, g, status, s);
+  else if (A.nc == 2 && g.np == 18) factorize_dispatch<18, 2, 6, 6>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 81) factorize_dispatch<81, 3, 9, 27>(A, g, status, s);
 }
 
 void launch_vanka_apply(const DevPatchGroup& g, int nc, const double* d, double* Y,
