@@ -87,6 +87,35 @@ int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nn
                          int64_t nnz_pp, const int64_t* pp_indptr, const int32_t* pp_indices,
                          const double* pp_data);
 
+/* Operator structure only (data zeroed on the device), for device assembly. */
+int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nnzb,
+                          const int64_t* indptr, const int32_t* indices, int64_t nnz_pp,
+                          const int64_t* pp_indptr, const int32_t* pp_indices);
+
+/* Device assembly of the condensed Jacobian (model.momentum_jacobian_data,
+ * reference model.py:297-381).  asm_setup (once per level): Q2 cell nodes
+ * (n_cells, 3^dim) int32, node coordinates (n_nodes, dim), cells grouped by
+ * colour (group_kind 0 fluid / 1 solid; a colour's cells share no node), the
+ * LPS macro entries as (cell slot | -1, pp slot | -1, value) triples
+ * (problem.py:79-90) and the Dirichlet row mask (n_nodes*nc bytes).
+ * asm_tables: Q2 basis N (nq,nb), gradients dN (nq,nb,dim), weights (nq).
+ * asm_momentum: params = {rho_f, mu_f, rho_s, mu_s, lam_s, k, theta}; U and
+ * U_prev host (n_nodes, 1+2dim); extra = host-reduced outflow-facet blocks
+ * (unique slots).  The matrix must be re-factorised afterwards. */
+int alefsi_mg_asm_setup(alefsi_mg h, int32_t level, int32_t dim, int64_t n_cells,
+                        const int32_t* cell_nodes, const double* coords, int32_t n_groups,
+                        const int64_t* group_ptr, const int32_t* group_kind,
+                        const int32_t* group_cells, int64_t n_lps, const int64_t* lps_cell_slot,
+                        const int64_t* lps_pp_slot, const double* lps_vals,
+                        const uint8_t* dirichlet);
+int alefsi_mg_asm_tables(alefsi_mg h, int32_t dim, int32_t nq, const double* N, const double* dN,
+                         const double* w);
+int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, const double* U,
+                           const double* U_prev, int64_t n_extra, const int64_t* extra_slots,
+                           const double* extra_vals);
+/* Copy a level's operator data (blocks, pp entries) to host memory. */
+int alefsi_mg_get_matrix(alefsi_mg h, int32_t level, double* data, double* pp_data);
+
 /* PatchSet groups (reference mesh.py:446-480): n_groups homogeneous groups,
  * patch_nodes concatenated group after group (node ids, patch-major).
  * HOST pointers. */

@@ -50,6 +50,11 @@ SIGNATURES = {
     "alefsi_gmres": [_p, _p, _p, _f64, _f64, _i32, _i32, _p, _p, _p],
     "alefsi_gmres_workspace": [_p, _i32],
     "alefsi_kernel_stats": [_p, _p],
+    "alefsi_mg_set_pattern": [_p, _i32, _i64, _i64, _p, _p, _i64, _p, _p],
+    "alefsi_mg_asm_setup": [_p, _i32, _i32, _i64, _p, _p, _i32, _p, _p, _p, _i64, _p, _p, _p, _p],
+    "alefsi_mg_asm_tables": [_p, _i32, _i32, _p, _p, _p],
+    "alefsi_mg_asm_momentum": [_p, _i32, _p, _p, _p, _i64, _p, _p],
+    "alefsi_mg_get_matrix": [_p, _i32, _p, _p],
     "alefsi_mg_profile": [_p, _i32],
     "alefsi_mg_profile_read": [_p, _p, _p, _i32],
 }

@@ -1,0 +1,428 @@
+// Device assembly of the condensed velocity-pressure Jacobian, sm_100a, FP64.
+//
+// Restates reference pkg/src/alefsi/model.py:297-361 (momentum_jacobian_data,
+// fluid and solid cells) directly into the split block layout in HBM: one CTA
+// per Q2 cell, isoparametric geometry recomputed from the node coordinates,
+// quadrature-point kinematics staged in shared memory, the 27x27 (9x9) local
+// block matrix accumulated in registers and added into the block-CSR data.
+// Cells are launched colour by colour (no two cells of a colour share a
+// node), so the accumulation needs no atomics and is deterministic.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "assembly_kernels.cuh"
+
+namespace alefsi {
+namespace {
+
+constexpr int kMaxQ = 27, kMaxB = 27;
+__constant__ double cN[kMaxQ * kMaxB];          // N[q][b]
+__constant__ double cdN[kMaxQ * kMaxB * 3];     // dN[q][b][j]
+__constant__ double cW[kMaxQ];                  // Gauss weights
+
+template <int D>
+__device__ __forceinline__ double det(const double (&A)[D][D]) {
+  if constexpr (D == 2) return A[0][0] * A[1][1] - A[0][1] * A[1][0];
+  else
+    return A[0][0] * (A[1][1] * A[2][2] - A[1][2] * A[2][1]) -
+           A[0][1] * (A[1][0] * A[2][2] - A[1][2] * A[2][0]) +
+           A[0][2] * (A[1][0] * A[2][1] - A[1][1] * A[2][0]);
+}
+
+template <int D>
+__device__ __forceinline__ void inv(const double (&A)[D][D], double (&R)[D][D], double dt) {
+  const double r = 1.0 / dt;
+  if constexpr (D == 2) {
+    R[0][0] = A[1][1] * r;
+    R[0][1] = -A[0][1] * r;
+    R[1][0] = -A[1][0] * r;
+    R[1][1] = A[0][0] * r;
+  } else {
+    R[0][0] = (A[1][1] * A[2][2] - A[1][2] * A[2][1]) * r;
+    R[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) * r;
+    R[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) * r;
+    R[1][0] = (A[1][2] * A[2][0] - A[1][0] * A[2][2]) * r;
+    R[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) * r;
+    R[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) * r;
+    R[2][0] = (A[1][0] * A[2][1] - A[1][1] * A[2][0]) * r;
+    R[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) * r;
+    R[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) * r;
+  }
+}
+
+// Shared per-cell tables (sizes for D=3; D=2 uses the leading part).
+struct CellShared {
+  double X[kMaxB][3];
+  double U[kMaxB][7], Up[kMaxB][7];
+  double G[kMaxQ][kMaxB][3];        // physical basis gradients
+  double T[kMaxQ][kMaxB][3];        // fluid: F^-T G_a;  solid: F G_a
+  double S[kMaxQ][kMaxB][3];        // fluid: G_b K;     solid: G_a Sigma
+  double coef[kMaxQ][kMaxB];        // fluid convection coefficient of trial a
+  double M[kMaxQ][9];               // fluid: grad v F^-1;  solid: F F^T
+  double s[kMaxQ][6];               // per-q weights
+  double Jinv[kMaxQ][9];
+  int slot[kMaxB * kMaxB];
+  int bad;
+};
+
+// KIND 0: fluid cells (model.py:303-337), 1: solid cells (model.py:339-361).
+template <int D, int KIND>
+__global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const int32_t* cells,
+                                                             int64_t n_cells) {
+  constexpr int NB = (D == 3) ? 27 : 9, NQ = NB, NC = D + 1, NF = 1 + 2 * D;
+  extern __shared__ double smem_raw[];
+  CellShared& sh = *reinterpret_cast<CellShared*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int64_t cell = cells[blockIdx.x];
+  const int32_t* cn = a.cell_nodes + cell * NB;
+  if (tid == 0) sh.bad = 0;
+  for (int t = tid; t < NB * D; t += blockDim.x) sh.X[t / D][t % D] = a.coords[(int64_t)cn[t / D] * D + t % D];
+  for (int t = tid; t < NB * NF; t += blockDim.x) {
+    const int b = t / NF, f = t - b * NF;
+    sh.U[b][f] = a.U[(int64_t)cn[b] * NF + f];
+    sh.Up[b][f] = a.Up[(int64_t)cn[b] * NF + f];
+  }
+  // block slots of every (row b, column a) node pair
+  for (int t = tid; t < NB * NB; t += blockDim.x) {
+    const int b = t / NB, c = t - b * NB;
+    const int64_t row = cn[b];
+    const int32_t col = cn[c];
+    int64_t lo = a.indptr[row], hi = a.indptr[row + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (a.indices[mid] < col) lo = mid + 1; else hi = mid;
+    }
+    sh.slot[t] = (int)lo;
+  }
+  __syncthreads();
+  // geometry: J = sum_b X_b (x) dN_b, its inverse and weighted determinant
+  if (tid < NQ) {
+    const int q = tid;
+    double J[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double acc = 0.0;
+        for (int b = 0; b < NB; ++b) acc += sh.X[b][i] * cdN[(q * NB + b) * 3 + j];
+        J[i][j] = acc;
+      }
+    const double dt = det<D>(J);
+    if (!(dt > 0.0)) sh.bad = 1;
+    double Ji[D][D];
+    inv<D>(J, Ji, dt);
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) sh.Jinv[q][i * D + j] = Ji[i][j];
+    sh.s[q][5] = dt * cW[q];
+  }
+  __syncthreads();
+  for (int t = tid; t < NQ * NB; t += blockDim.x) {
+    const int q = t / NB, b = t - q * NB;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc += cdN[(q * NB + b) * 3 + j] * sh.Jinv[q][j * D + i];
+      sh.G[q][b][i] = acc;
+    }
+  }
+  __syncthreads();
+  // quadrature-point kinematics
+  if (tid < NQ) {
+    const int q = tid;
+    double v[D], u[D], up[D], gv[D][D], gu[D][D], gvp[D][D], gup[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      v[i] = u[i] = up[i] = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) gv[i][j] = gu[i][j] = gvp[i][j] = gup[i][j] = 0.0;
+    }
+    for (int b = 0; b < NB; ++b) {
+      const double nb = cN[q * NB + b];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        v[i] += nb * sh.U[b][1 + i];
+        u[i] += nb * sh.U[b][1 + D + i];
+        up[i] += nb * sh.Up[b][1 + D + i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double g = sh.G[q][b][j];
+          gv[i][j] += g * sh.U[b][1 + i];
+          gu[i][j] += g * sh.U[b][1 + D + i];
+          gvp[i][j] += g * sh.Up[b][1 + i];
+          gup[i][j] += g * sh.Up[b][1 + D + i];
+        }
+      }
+    }
+    const double w = sh.s[q][5];
+    if constexpr (KIND == 0) {
+      double F[D][D], Fp[D][D], Fb[D][D], Fi[D][D], Fbi[D][D];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          F[i][j] = gu[i][j] + (i == j ? 1.0 : 0.0);
+          Fp[i][j] = gup[i][j] + (i == j ? 1.0 : 0.0);
+          Fb[i][j] = 0.5 * (F[i][j] + Fp[i][j]);
+        }
+      const double J = det<D>(F), Jp = det<D>(Fp);
+      if (!(J > 0.0) || !(Jp > 0.0)) sh.bad = 2;
+      inv<D>(F, Fi, J);
+      inv<D>(Fb, Fbi, det<D>(Fb));
+      const double Jbar = 0.5 * (J + Jp);
+      double wv[D], Fiv[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        wv[i] = 0.0;
+        Fiv[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          wv[i] += Fbi[i][j] * (u[j] - up[j]);
+          Fiv[i] += Fi[i][j] * v[j];
+        }
+      }
+      // grad v F^-1 and K = F^-1 F^-T
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double g = 0.0, kk = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) {
+            g += gv[i][m] * Fi[m][j];
+            kk += Fi[i][m] * Fi[j][m];
+          }
+          sh.M[q][i * D + j] = g;
+          sh.Jinv[q][i * D + j] = kk;  // reuse as K
+        }
+      const double kt = a.k * a.theta;
+      sh.s[q][0] = w * a.rho_f * Jbar;          // mass
+      sh.s[q][1] = w * kt * a.mu_f * J;          // viscous
+      sh.s[q][2] = w * kt * a.rho_f * J;         // convection
+      sh.s[q][3] = w * (-a.k) * J;               // pressure column
+      sh.s[q][4] = w * a.k * J;                  // divergence row
+      // per trial function a: F^-T G_a, coefficient, G_a K
+      for (int b = 0; b < NB; ++b) {
+        double gw = 0.0, gf = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double t = 0.0, s = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) {
+            t += Fi[m][i] * sh.G[q][b][m];
+            s += sh.G[q][b][m] * sh.Jinv[q][m * D + i];
+          }
+          sh.T[q][b][i] = t;
+          sh.S[q][b][i] = s;
+          gw += sh.G[q][b][i] * wv[i];
+          gf += sh.G[q][b][i] * Fiv[i];
+        }
+        sh.coef[q][b] = w * ((-0.5 * a.rho_f * Jbar) * gw + (kt * a.rho_f * J) * gf);
+      }
+    } else {
+      double F[D][D], E[D][D];
+      const double kt = a.k * a.theta;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+          F[i][j] = gup[i][j] + kt * gv[i][j] + a.k * (1.0 - a.theta) * gvp[i][j] +
+                    (i == j ? 1.0 : 0.0);
+      if (!(det<D>(F) > 0.0)) sh.bad = 3;
+      double tr = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double e = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) e += F[m][i] * F[m][j];
+          E[i][j] = 0.5 * (e - (i == j ? 1.0 : 0.0));
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i) tr += E[i][i];
+      double Sig[D][D];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+          Sig[i][j] = 2.0 * a.mu_s * E[i][j] + (i == j ? a.lam_s * tr : 0.0);
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double ff = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) ff += F[i][m] * F[j][m];
+          sh.M[q][i * D + j] = ff;            // F F^T
+        }
+      const double kt2 = kt * kt;
+      sh.s[q][0] = w * a.rho_s;
+      sh.s[q][1] = w * kt2;
+      sh.s[q][2] = w * kt2 * a.mu_s;
+      sh.s[q][3] = w * kt2 * a.lam_s;
+      for (int b = 0; b < NB; ++b) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double t = 0.0, s = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) {
+            t += F[i][m] * sh.G[q][b][m];
+            s += sh.G[q][b][m] * Sig[m][i];
+          }
+          sh.T[q][b][i] = t;       // (F G_b)_i
+          sh.S[q][b][i] = s;       // (G_b Sigma)_i
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (sh.bad) {
+    if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(a.status), 0ull,
+                            (unsigned long long)(cell + 1));
+    return;
+  }
+  // local blocks: thread per (row b, column a) pair
+  for (int t = tid; t < NB * NB; t += blockDim.x) {
+    const int b = t / NB, c = t - b * NB;   // c = trial function "a"
+    double blk[NC][NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) blk[i][j] = 0.0;
+    double diag = 0.0;
+    for (int q = 0; q < NQ; ++q) {
+      const double nb = cN[q * NB + b], na = cN[q * NB + c];
+      if constexpr (KIND == 0) {
+        double gkg = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) gkg += sh.S[q][b][m] * sh.G[q][c][m];
+        diag += nb * sh.coef[q][c] + sh.s[q][0] * nb * na + sh.s[q][1] * gkg;
+        const double cnn = sh.s[q][2] * nb * na;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+#pragma unroll
+          for (int j = 0; j < D; ++j)
+            blk[1 + i][1 + j] += cnn * sh.M[q][i * D + j] + sh.s[q][1] * sh.T[q][c][i] * sh.T[q][b][j];
+          blk[1 + i][0] += sh.s[q][3] * na * sh.T[q][b][i];
+          blk[0][1 + i] += sh.s[q][4] * nb * sh.T[q][c][i];
+        }
+      } else {
+        double gsg = 0.0, gg = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+          gsg += sh.S[q][c][m] * sh.G[q][b][m];
+          gg += sh.G[q][c][m] * sh.G[q][b][m];
+        }
+        diag += sh.s[q][0] * nb * na + sh.s[q][1] * gsg;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j)
+            blk[1 + i][1 + j] += sh.s[q][2] * (sh.T[q][c][i] * sh.T[q][b][j] + sh.M[q][i * D + j] * gg) +
+                                 sh.s[q][3] * sh.T[q][b][i] * sh.T[q][c][j];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) blk[1 + i][1 + i] += diag;
+    double* dst = a.data + (int64_t)sh.slot[t] * (NC * NC);
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+      for (int j = 0; j < NC; ++j) dst[i * NC + j] += blk[i][j];
+  }
+}
+
+// data[slot] += vals (unique slots; host-reduced facet contributions)
+__global__ void add_blocks_kernel(double* data, int bs, int64_t n, const int64_t* slots,
+                                  const double* vals) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * bs) return;
+  const int64_t e = t / bs;
+  const int c = (int)(t - e * bs);
+  data[slots[e] * bs + c] += vals[t];
+}
+
+// LPS: data[cell_slot](0,0) += k*val  /  pp[pp_slot] = k*val (problem.py:79-90)
+__global__ void lps_kernel(double* data, int nc, double* pp, int64_t n, const int64_t* cell_slot,
+                           const int64_t* pp_slot, const double* vals, double k) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const double v = k * vals[e];
+  if (cell_slot[e] >= 0) data[cell_slot[e] * nc * nc] += v;
+  else pp[pp_slot[e]] = v;
+}
+
+// Dirichlet rows -> identity rows (fem.py:172-182), one warp per node row
+__global__ void dirichlet_kernel(double* data, int nc, double* pp, int64_t n_nodes,
+                                 const int64_t* indptr, const int32_t* indices,
+                                 const int64_t* pp_indptr, const uint8_t* mask) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n_nodes) return;
+  for (int c = 0; c < nc; ++c) {
+    if (!mask[row * nc + c]) continue;
+    for (int64_t s = indptr[row] + lane; s < indptr[row + 1]; s += 32) {
+      double* blk = data + s * nc * nc + c * nc;
+      for (int j = 0; j < nc; ++j) blk[j] = (indices[s] == row && j == c) ? 1.0 : 0.0;
+    }
+    if (c == 0 && pp_indptr != nullptr)
+      for (int64_t s = pp_indptr[row] + lane; s < pp_indptr[row + 1]; s += 32) pp[s] = 0.0;
+  }
+}
+
+}  // namespace
+
+void set_assembly_tables(const double* N, const double* dN, const double* w, int nq, int nb,
+                         int dim) {
+  static double hdN[kMaxQ * kMaxB * 3];
+  for (int q = 0; q < nq; ++q)
+    for (int b = 0; b < nb; ++b)
+      for (int j = 0; j < 3; ++j) hdN[(q * nb + b) * 3 + j] = j < dim ? dN[(q * nb + b) * dim + j] : 0.0;
+  cudaMemcpyToSymbol(cN, N, sizeof(double) * nq * nb);
+  cudaMemcpyToSymbol(cdN, hdN, sizeof(double) * nq * nb * 3);
+  cudaMemcpyToSymbol(cW, w, sizeof(double) * nq);
+}
+
+void launch_assemble_cells(const AsmArgs& a, int dim, int kind, const int32_t* cells,
+                           int64_t n_cells, cudaStream_t s) {
+  if (n_cells == 0) return;
+  const size_t smem = sizeof(CellShared);
+  if (dim == 3 && kind == 0) {
+    cudaFuncSetAttribute(assemble_cells_kernel<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    assemble_cells_kernel<3, 0><<<(unsigned)n_cells, 256, smem, s>>>(a, cells, n_cells);
+  } else if (dim == 3) {
+    cudaFuncSetAttribute(assemble_cells_kernel<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    assemble_cells_kernel<3, 1><<<(unsigned)n_cells, 256, smem, s>>>(a, cells, n_cells);
+  } else if (kind == 0) {
+    cudaFuncSetAttribute(assemble_cells_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    assemble_cells_kernel<2, 0><<<(unsigned)n_cells, 128, smem, s>>>(a, cells, n_cells);
+  } else {
+    cudaFuncSetAttribute(assemble_cells_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    assemble_cells_kernel<2, 1><<<(unsigned)n_cells, 128, smem, s>>>(a, cells, n_cells);
+  }
+}
+
+void launch_add_blocks(double* data, int bs, int64_t n, const int64_t* slots, const double* vals,
+                       cudaStream_t s) {
+  if (n == 0) return;
+  add_blocks_kernel<<<(unsigned)((n * bs + 255) / 256), 256, 0, s>>>(data, bs, n, slots, vals);
+}
+
+void launch_lps(double* data, int nc, double* pp, int64_t n, const int64_t* cell_slot,
+                const int64_t* pp_slot, const double* vals, double k, cudaStream_t s) {
+  if (n == 0) return;
+  lps_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(data, nc, pp, n, cell_slot, pp_slot, vals, k);
+}
+
+void launch_dirichlet(double* data, int nc, double* pp, int64_t n_nodes, const int64_t* indptr,
+                      const int32_t* indices, const int64_t* pp_indptr, const uint8_t* mask,
+                      cudaStream_t s) {
+  dirichlet_kernel<<<(unsigned)((n_nodes * 32 + 255) / 256), 256, 0, s>>>(
+      data, nc, pp, n_nodes, indptr, indices, pp_indptr, mask);
+}
+
+}  // namespace alefsi

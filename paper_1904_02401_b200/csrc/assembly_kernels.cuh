@@ -1,0 +1,34 @@
+// Device assembly of the condensed Jacobian (see assembly_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace alefsi {
+
+struct AsmArgs {
+  const int32_t* cell_nodes = nullptr;   // (n_cells, 3^d)
+  const double* coords = nullptr;        // (n_nodes, d)
+  const double* U = nullptr;             // (n_nodes, 1 + 2d) current state
+  const double* Up = nullptr;            // previous time step
+  const int64_t* indptr = nullptr;       // cell-stencil block pattern
+  const int32_t* indices = nullptr;
+  double* data = nullptr;                // (nnzb, d+1, d+1) output, accumulated
+  int64_t* status = nullptr;             // 1 + first inverted cell
+  double rho_f = 0, mu_f = 0, rho_s = 0, mu_s = 0, lam_s = 0, k = 0, theta = 0;
+};
+
+// Q2 tables at the Gauss points: N (nq, nb), dN (nq, nb, dim), weights (nq)
+void set_assembly_tables(const double* N, const double* dN, const double* w, int nq, int nb,
+                         int dim);
+// kind 0: fluid cells, 1: solid cells; cells of one colour (no shared nodes)
+void launch_assemble_cells(const AsmArgs& a, int dim, int kind, const int32_t* cells,
+                           int64_t n_cells, cudaStream_t s);
+void launch_add_blocks(double* data, int bs, int64_t n, const int64_t* slots, const double* vals,
+                       cudaStream_t s);
+void launch_lps(double* data, int nc, double* pp, int64_t n, const int64_t* cell_slot,
+                const int64_t* pp_slot, const double* vals, double k, cudaStream_t s);
+void launch_dirichlet(double* data, int nc, double* pp, int64_t n_nodes, const int64_t* indptr,
+                      const int32_t* indices, const int64_t* pp_indptr, const uint8_t* mask,
+                      cudaStream_t s);
+
+}  // namespace alefsi

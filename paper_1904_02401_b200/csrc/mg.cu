@@ -24,10 +24,33 @@
 
 #include "alefsi_common.h"
 #include "alefsi_b200.h"
+#include "assembly_kernels.cuh"
 #include "device_kernels.cuh"
 
 namespace alefsi {
 namespace {
+
+// dense (n*nc)^2 copy of a split operator (coarse level), warp per node row
+__global__ void split_to_dense_kernel(DevMatrix A, double* M) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= A.n_nodes) return;
+  const int nc = A.nc;
+  const int64_t n = A.n_nodes * nc;
+  for (int64_t s = A.indptr[row] + lane; s < A.indptr[row + 1]; s += 32) {
+    const int64_t col = A.indices[s];
+    for (int i = 0; i < nc; ++i)
+      for (int j = 0; j < nc; ++j)
+        M[(row * nc + i) * n + col * nc + j] += A.data[s * nc * nc + i * nc + j];
+  }
+  if (A.pp_indptr != nullptr)
+    for (int64_t s = A.pp_indptr[row] + lane; s < A.pp_indptr[row + 1]; s += 32)
+      M[(row * nc) * n + (int64_t)A.pp_indices[s] * nc] += A.pp_data[s];
+}
+
+void launch_split_to_dense(const DevMatrix& A, double* M, cudaStream_t s) {
+  split_to_dense_kernel<<<(unsigned)((A.n_nodes * 32 + 255) / 256), 256, 0, s>>>(A, M);
+}
 
 #define CK(expr)                                                                  \
   do {                                                                            \
@@ -103,6 +126,17 @@ struct Level {
   DevBuf<double> P_val, R_val;
   DevBuf<uint8_t> constrained;
   DevBuf<double> x, b, d;
+  // device assembly of the condensed Jacobian (assembly_kernels.cu)
+  bool has_asm = false;
+  int dim = 0;
+  DevBuf<int32_t> asm_cell_nodes, asm_group_cells;
+  DevBuf<double> asm_coords, asm_U, asm_Up;
+  std::vector<int64_t> asm_group_ptr;
+  std::vector<int> asm_group_kind;
+  int64_t n_lps = 0;
+  DevBuf<int64_t> lps_cell, lps_pp;
+  DevBuf<double> lps_val;
+  DevBuf<uint8_t> dir_mask;
 
   int64_t ndof() const { return n_nodes * nc; }
   DevMatrix mat() const {
@@ -353,7 +387,13 @@ struct MgHandle {
     Level& C = lv[0];
     if (!C.has_matrix) return fail(ALEFSI_ERR_STATE, "coarse matrix missing");
     const int64_t n0 = C.ndof();
-    CK(coarse_inv.upload(C.host_dense.data(), (size_t)n0 * n0, stream));
+    if (!C.host_dense.empty()) {
+      CK(coarse_inv.upload(C.host_dense.data(), (size_t)n0 * n0, stream));
+    } else {   // device-assembled coarse operator
+      CK(coarse_inv.alloc((size_t)n0 * n0));
+      CK(cudaMemsetAsync(coarse_inv.p, 0, sizeof(double) * n0 * n0, stream));
+      launch_split_to_dense(C.mat(), coarse_inv.p, stream);
+    }
     CK(coarse_work.alloc(2 * n0 + 2));
     dense_inverse(coarse_inv.p, n0, coarse_work.p, status.p, stream);
     CK(cudaGetLastError());
@@ -633,6 +673,167 @@ int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nn
   L.has_matrix = true;
   m->factorized = false;
   m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nnzb,
+                          const int64_t* indptr, const int32_t* indices, int64_t nnz_pp,
+                          const int64_t* pp_indptr, const int32_t* pp_indices) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  const int nc = m->nc;
+  if (indptr[0] != 0 || indptr[n_nodes] != nnzb) return fail(ALEFSI_ERR_ARG, "bad indptr");
+  if (nnzb >= (int64_t)1 << 31) return fail(ALEFSI_ERR_ARG, "pattern too large for int32 slots");
+  L.n_nodes = n_nodes;
+  L.nnzb = nnzb;
+  L.nnz_pp = nnz_pp;
+  CKAPI(L.indptr.upload(indptr, n_nodes + 1, m->stream));
+  CKAPI(L.indices.upload(indices, nnzb, m->stream));
+  CKAPI(L.data.alloc((size_t)nnzb * nc * nc));
+  CKAPI(cudaMemsetAsync(L.data.p, 0, sizeof(double) * nnzb * nc * nc, m->stream));
+  if (nnz_pp > 0) {
+    CKAPI(L.pp_indptr.upload(pp_indptr, n_nodes + 1, m->stream));
+    CKAPI(L.pp_indices.upload(pp_indices, nnz_pp, m->stream));
+    CKAPI(L.pp_data.alloc(nnz_pp));
+    CKAPI(cudaMemsetAsync(L.pp_data.p, 0, sizeof(double) * nnz_pp, m->stream));
+  }
+  L.host_dense.clear();
+  CKAPI(cudaStreamSynchronize(m->stream));
+  L.has_matrix = true;
+  m->factorized = false;
+  m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_asm_setup(alefsi_mg h, int32_t level, int32_t dim, int64_t n_cells,
+                        const int32_t* cell_nodes, const double* coords, int32_t n_groups,
+                        const int64_t* group_ptr, const int32_t* group_kind,
+                        const int32_t* group_cells, int64_t n_lps, const int64_t* lps_cell_slot,
+                        const int64_t* lps_pp_slot, const double* lps_vals,
+                        const uint8_t* dirichlet) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (!L.has_matrix) return fail(ALEFSI_ERR_STATE, "set_pattern before asm_setup");
+  if (dim + 1 != m->nc || (dim != 2 && dim != 3)) return fail(ALEFSI_ERR_ARG, "asm: bad dim");
+  const int nb = dim == 3 ? 27 : 9;
+  L.dim = dim;
+  CKAPI(L.asm_cell_nodes.upload(cell_nodes, (size_t)n_cells * nb, m->stream));
+  CKAPI(L.asm_coords.upload(coords, (size_t)L.n_nodes * dim, m->stream));
+  L.asm_group_ptr.assign(group_ptr, group_ptr + n_groups + 1);
+  L.asm_group_kind.assign(group_kind, group_kind + n_groups);
+  CKAPI(L.asm_group_cells.upload(group_cells, group_ptr[n_groups], m->stream));
+  L.n_lps = n_lps;
+  if (n_lps > 0) {
+    CKAPI(L.lps_cell.upload(lps_cell_slot, n_lps, m->stream));
+    CKAPI(L.lps_pp.upload(lps_pp_slot, n_lps, m->stream));
+    CKAPI(L.lps_val.upload(lps_vals, n_lps, m->stream));
+  }
+  CKAPI(L.dir_mask.upload(dirichlet, L.ndof(), m->stream));
+  CKAPI(L.asm_U.alloc((size_t)L.n_nodes * (1 + 2 * dim)));
+  CKAPI(L.asm_Up.alloc((size_t)L.n_nodes * (1 + 2 * dim)));
+  CKAPI(cudaStreamSynchronize(m->stream));
+  L.has_asm = true;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_asm_tables(alefsi_mg h, int32_t dim, int32_t nq, const double* N, const double* dN,
+                         const double* w) {
+  MgHandle* m = H(h);
+  if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
+  const int nb = dim == 3 ? 27 : 9;
+  if (nq > 27) return fail(ALEFSI_ERR_ARG, "asm: at most 27 quadrature points");
+  cudaStreamSynchronize(m->stream);
+  alefsi::set_assembly_tables(N, dN, w, nq, nb, dim);
+  CKAPI(cudaGetLastError());
+  return ALEFSI_OK;
+}
+
+// params = rho_f, mu_f, rho_s, mu_s, lam_s, k, theta; U, Up host (n_nodes, 1+2d);
+// extra = host-reduced facet blocks (unique slots) added after the cells
+int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, const double* U,
+                           const double* Up, int64_t n_extra, const int64_t* extra_slots,
+                           const double* extra_vals) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (!L.has_asm) return fail(ALEFSI_ERR_STATE, "asm_setup missing");
+  const int nc = m->nc, nf = 1 + 2 * L.dim;
+  cudaStream_t s = m->stream;
+  CKAPI(cudaMemcpyAsync(L.asm_U.p, U, sizeof(double) * L.n_nodes * nf, cudaMemcpyHostToDevice, s));
+  CKAPI(cudaMemcpyAsync(L.asm_Up.p, Up, sizeof(double) * L.n_nodes * nf, cudaMemcpyHostToDevice, s));
+  CKAPI(cudaMemsetAsync(L.data.p, 0, sizeof(double) * L.nnzb * nc * nc, s));
+  if (L.nnz_pp > 0) CKAPI(cudaMemsetAsync(L.pp_data.p, 0, sizeof(double) * L.nnz_pp, s));
+  CKAPI(cudaMemsetAsync(m->status.p, 0, sizeof(int64_t), s));
+  alefsi::AsmArgs a;
+  a.cell_nodes = L.asm_cell_nodes.p;
+  a.coords = L.asm_coords.p;
+  a.U = L.asm_U.p;
+  a.Up = L.asm_Up.p;
+  a.indptr = L.indptr.p;
+  a.indices = L.indices.p;
+  a.data = L.data.p;
+  a.status = m->status.p;
+  a.rho_f = params[0];
+  a.mu_f = params[1];
+  a.rho_s = params[2];
+  a.mu_s = params[3];
+  a.lam_s = params[4];
+  a.k = params[5];
+  a.theta = params[6];
+  for (size_t g = 0; g + 1 < L.asm_group_ptr.size(); ++g) {
+    const int64_t b = L.asm_group_ptr[g], e = L.asm_group_ptr[g + 1];
+    alefsi::launch_assemble_cells(a, L.dim, L.asm_group_kind[g], L.asm_group_cells.p + b, e - b, s);
+    ++m->kernel_launches;
+  }
+  CKAPI(cudaGetLastError());
+  if (n_extra > 0) {
+    alefsi::DevBuf<int64_t> sl;
+    alefsi::DevBuf<double> vv;
+    CKAPI(sl.upload(extra_slots, n_extra, s));
+    CKAPI(vv.upload(extra_vals, (size_t)n_extra * nc * nc, s));
+    alefsi::launch_add_blocks(L.data.p, nc * nc, n_extra, sl.p, vv.p, s);
+    CKAPI(cudaStreamSynchronize(s));
+  }
+  alefsi::launch_lps(L.data.p, nc, L.pp_data.p, L.n_lps, L.lps_cell.p, L.lps_pp.p, L.lps_val.p,
+                     a.k, s);
+  alefsi::launch_dirichlet(L.data.p, nc, L.pp_data.p, L.n_nodes, L.indptr.p, L.indices.p,
+                           L.nnz_pp > 0 ? L.pp_indptr.p : nullptr, L.dir_mask.p, s);
+  m->kernel_launches += 2;
+  int64_t st = 0;
+  CKAPI(cudaMemcpyAsync(&st, m->status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CKAPI(cudaStreamSynchronize(s));
+  if (st != 0)
+    return fail(ALEFSI_ERR_SINGULAR, "inverted element in device assembly: cell " +
+                                         std::to_string(st - 1));
+  m->factorized = false;
+  m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_get_matrix(alefsi_mg h, int32_t level, double* data, double* pp_data) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  CKAPI(cudaMemcpyAsync(data, L.data.p, sizeof(double) * L.nnzb * m->nc * m->nc,
+                        cudaMemcpyDeviceToHost, m->stream));
+  if (L.nnz_pp > 0 && pp_data)
+    CKAPI(cudaMemcpyAsync(pp_data, L.pp_data.p, sizeof(double) * L.nnz_pp,
+                          cudaMemcpyDeviceToHost, m->stream));
+  CKAPI(cudaStreamSynchronize(m->stream));
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }

@@ -48,10 +48,11 @@ class DeviceMgSolver:
     prolongation from the coarser level; None on level 0) and
     ``constrained`` (bool per dof)."""
 
-    def __init__(self, levels, nu_pre=2, nu_post=2, omega=0.8, use_graph=False, stream=None):
+    def __init__(self, levels, nu_pre=2, nu_post=2, omega=0.8, use_graph=False, stream=None,
+                 factorize=True, nc=None):
         lib = _lib.load()
         self.n_levels = len(levels)
-        self.nc = levels[0]["matrix"].nc
+        self.nc = nc if nc is not None else levels[0]["matrix"].nc
         self.nu_pre, self.nu_post, self.omega = nu_pre, nu_post, omega
         h = C.c_void_p()
         _lib.call("alefsi_mg_create", self.n_levels, self.nc, nu_pre, nu_post, float(omega),
@@ -74,20 +75,30 @@ class DeviceMgSolver:
         for l, lv in enumerate(levels):
             self._set_level(l, lv)
         _lib.call("alefsi_mg_use_graph", h, 1 if use_graph else 0)
-        self.factorize()
+        if factorize:
+            self.factorize()
 
     # -- setup ------------------------------------------------------------------
     def _set_level(self, l, lv):
-        A = lv["matrix"]
-        p = A.pattern
-        _lib.call("alefsi_mg_set_matrix", self._h, l, p.n_nodes, p.nnzb,
-                  np.ascontiguousarray(p.indptr, dtype=np.int64),
-                  np.ascontiguousarray(p.indices, dtype=np.int32),
-                  np.ascontiguousarray(A.data, dtype=np.float64), p.nnz_pp,
-                  np.ascontiguousarray(p.pp_indptr, dtype=np.int64),
-                  np.ascontiguousarray(p.pp_indices, dtype=np.int32),
-                  np.ascontiguousarray(A.pp_data, dtype=np.float64))
-        self.ndofs.append(p.n_nodes * A.nc)
+        A = lv.get("matrix")
+        if A is None:          # structure only: the operator is assembled on the device
+            p = lv["pattern"]
+            _lib.call("alefsi_mg_set_pattern", self._h, l, p.n_nodes, p.nnzb,
+                      np.ascontiguousarray(p.indptr, dtype=np.int64),
+                      np.ascontiguousarray(p.indices, dtype=np.int32), p.nnz_pp,
+                      np.ascontiguousarray(p.pp_indptr, dtype=np.int64),
+                      np.ascontiguousarray(p.pp_indices, dtype=np.int32))
+            self.ndofs.append(p.n_nodes * self.nc)
+        else:
+            p = A.pattern
+            _lib.call("alefsi_mg_set_matrix", self._h, l, p.n_nodes, p.nnzb,
+                      np.ascontiguousarray(p.indptr, dtype=np.int64),
+                      np.ascontiguousarray(p.indices, dtype=np.int32),
+                      np.ascontiguousarray(A.data, dtype=np.float64), p.nnz_pp,
+                      np.ascontiguousarray(p.pp_indptr, dtype=np.int64),
+                      np.ascontiguousarray(p.pp_indices, dtype=np.int32),
+                      np.ascontiguousarray(A.pp_data, dtype=np.float64))
+            self.ndofs.append(p.n_nodes * A.nc)
         mask = np.ascontiguousarray(np.asarray(lv["constrained"]).reshape(-1), dtype=np.uint8)
         _lib.call("alefsi_mg_set_constrained", self._h, l, mask)
         if l == 0:
@@ -231,6 +242,68 @@ class DeviceMgSolver:
 
     def reserve(self, max_iter):
         _lib.call("alefsi_gmres_workspace", self._h, int(max_iter))
+
+    # -- device assembly of the condensed Jacobian -----------------------------------
+    def asm_setup(self, level, lvl):
+        """Upload cell topology, geometry, colour groups, LPS entries and the
+        Dirichlet mask of one LevelData for device assembly."""
+        from . import mesh as mm
+        m = lvl.mesh
+        d = lvl.dim
+        groups, kinds = [], []
+        for cells, kind in ((lvl.fluid_cells, 0), (lvl.solid_cells, 1)):
+            if len(cells) == 0:
+                continue
+            ps = mm.PatchSet(n_comp=1)
+            ps.add(m.cell_nodes[cells], 0)
+            col = mm.color_patches(ps)
+            for c in range(col.n_colors):
+                groups.append(cells[col.color == c])
+                kinds.append(kind)
+        gptr = np.concatenate([[0], np.cumsum([len(g) for g in groups])]).astype(np.int64)
+        gcells = np.ascontiguousarray(np.concatenate(groups), dtype=np.int32)
+        p = lvl.pattern
+        _lib.call("alefsi_mg_asm_setup", self._h, level, d, len(m.cells),
+                  np.ascontiguousarray(m.cell_nodes, dtype=np.int32),
+                  np.ascontiguousarray(m.nodes, dtype=np.float64), len(groups), gptr,
+                  np.asarray(kinds, dtype=np.int32), gcells, len(p.macro_to_cell),
+                  np.ascontiguousarray(p.macro_to_cell, dtype=np.int64),
+                  np.ascontiguousarray(p.macro_to_pp, dtype=np.int64),
+                  np.ascontiguousarray(lvl.lps_macro_vals, dtype=np.float64),
+                  np.ascontiguousarray(lvl.momentum_dirichlet.reshape(-1), dtype=np.uint8))
+        t = lvl.table
+        _lib.call("alefsi_mg_asm_tables", self._h, d, t.N.shape[0],
+                  np.ascontiguousarray(t.N), np.ascontiguousarray(t.dN),
+                  np.ascontiguousarray(lvl.quad_weights))
+
+    def asm_momentum(self, level, lvl, mats, k, theta, U, U_prev):
+        """Assemble the condensed Jacobian of one level on the device (cells,
+        outflow facets, LPS, Dirichlet rows); refactorise afterwards."""
+        from . import fem, model
+        d = lvl.dim
+        nc = d + 1
+        slots = np.zeros(0, dtype=np.int64)
+        vals = np.zeros((0, nc, nc))
+        if lvl.outflow is not None:
+            with fem.single_blas():
+                local = model._outflow_blocks(lvl.outflow, U, mats, k, theta, d)
+            sl = fem.pattern_slots(lvl.pattern.indptr, lvl.pattern.indices,
+                                   lvl.outflow.conn).reshape(-1)
+            slots, inv = np.unique(sl, return_inverse=True)
+            vals = np.zeros((len(slots), nc, nc))
+            np.add.at(vals, inv, local.reshape(-1, nc, nc))
+        params = np.array([mats.rho_f, mats.mu_f, mats.rho_s, mats.mu_s, mats.lam_s, k, theta])
+        _lib.call("alefsi_mg_asm_momentum", self._h, level, params,
+                  np.ascontiguousarray(U, dtype=np.float64),
+                  np.ascontiguousarray(U_prev, dtype=np.float64), len(slots),
+                  np.ascontiguousarray(slots, dtype=np.int64),
+                  np.ascontiguousarray(vals, dtype=np.float64))
+
+    def matrix_data(self, level, pattern):
+        data = np.empty((pattern.nnzb, self.nc, self.nc))
+        pp = np.empty(pattern.nnz_pp)
+        _lib.call("alefsi_mg_get_matrix", self._h, level, data, pp)
+        return data, pp
 
     # -- construction from a workload case -------------------------------------------
     @classmethod

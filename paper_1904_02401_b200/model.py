@@ -50,10 +50,11 @@ class MaterialParams:
 
 def _fields(G, N, Uc, d):
     """Values and gradients of v (comps 1..d) and u (comps d+1..2d) at qpoints."""
-    v = np.einsum("qb,cbi->cqi", N, Uc[:, :, 1:1 + d])
-    u = np.einsum("qb,cbi->cqi", N, Uc[:, :, 1 + d:])
-    gv = np.einsum("cqbj,cbi->cqij", G, Uc[:, :, 1:1 + d], optimize=True)
-    gu = np.einsum("cqbj,cbi->cqij", G, Uc[:, :, 1 + d:], optimize=True)
+    v = np.matmul(N[None], Uc[:, :, 1:1 + d])
+    u = np.matmul(N[None], Uc[:, :, 1 + d:])
+    GT = np.swapaxes(G, 2, 3)                                  # (c, q, j, b)
+    gv = np.swapaxes(np.matmul(GT, Uc[:, None, :, 1:1 + d]), 2, 3)
+    gu = np.swapaxes(np.matmul(GT, Uc[:, None, :, 1 + d:]), 2, 3)
     return v, u, gv, gu
 
 
@@ -195,9 +196,10 @@ def _test(wdet, N, G, val, grad):
     """sum_q w (N_b val_i + G_b . grad_i) -> (c, b, i) (model.py:147-154)."""
     out = 0.0
     if val is not None:
-        out = out + np.einsum("cq,qb,cqi->cbi", wdet, N, val, optimize=True)
+        out = out + np.matmul(N.T[None], wdet[:, :, None] * val)
     if grad is not None:
-        out = out + np.einsum("cq,cqbj,cqij->cbi", wdet, G, grad, optimize=True)
+        wg = np.swapaxes(grad * wdet[:, :, None, None], 2, 3)      # (c, q, j, i)
+        out = out + np.matmul(G, wg).sum(axis=1)
     return out
 
 
@@ -231,8 +233,8 @@ def explicit_forces(lvl, mats, flags, U_prev):
     d = lvl.dim
     X = np.zeros((lvl.n_nodes, d))
     f = np.asarray(mats.body_force, dtype=float)
-    cells = lvl.fluid_cells
-    if len(cells):
+
+    def fluid_local(cells):
         _, v, _, gv, gu = _qfields(lvl, cells, U_prev)
         _, J, Fi = _fluid_kin(gu)
         gvFi = gv @ Fi
@@ -240,16 +242,18 @@ def explicit_forces(lvl, mats, flags, U_prev):
         conv = conv - mats.rho_f * J[..., None] * f
         visc = mats.mu_f * J[..., None, None] * ((gvFi + np.swapaxes(gvFi, -1, -2))
                                                  @ np.swapaxes(Fi, -1, -2))
-        np.add.at(X, lvl.mesh.cell_nodes[cells],
-                  _test(lvl.wdet[cells], lvl.table.N, lvl.G[cells], conv, visc))
-    cells = lvl.solid_cells
-    if len(cells):
+        return _test(lvl.wdet[cells], lvl.table.N, lvl.G[cells], conv, visc)
+
+    def solid_local(cells):
         _, v, _, _, gu = _qfields(lvl, cells, U_prev)
         F, _, _, E = kinematics(gu)
         sval = -mats.rho_s * np.broadcast_to(f, v.shape)
-        np.add.at(X, lvl.mesh.cell_nodes[cells],
-                  _test(lvl.wdet[cells], lvl.table.N, lvl.G[cells], sval, _svk(F, E, mats)))
-    outflow_correction(lvl, mats, U_prev, X)
+        return _test(lvl.wdet[cells], lvl.table.N, lvl.G[cells], sval, _svk(F, E, mats))
+
+    with fem.single_blas():
+        _chunked_scatter(lvl, lvl.fluid_cells, fluid_local, X)
+        _chunked_scatter(lvl, lvl.solid_cells, solid_local, X)
+        outflow_correction(lvl, mats, U_prev, X)
     return X
 
 
@@ -260,6 +264,20 @@ def theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit=None):
         return _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit)
 
 
+def _chunked_scatter(lvl, cells, fn, out, chunk=1024):
+    """out[conn] += fn(cell chunk) over chunks computed on a thread pool and
+    accumulated in chunk order (same order as one np.add.at over all cells)."""
+    conn = lvl.mesh.cell_nodes
+
+    def work(s):
+        c = cells[s:s + chunk]
+        return c, fn(c)
+
+    def consume(res):
+        np.add.at(out, conn[res[0]], res[1])
+    fem.parallel_chunks(work, range(0, len(cells), chunk), consume)
+
+
 def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
     d = lvl.dim
     n = lvl.n_nodes
@@ -268,8 +286,8 @@ def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
     R = np.zeros((n, 1 + 2 * d))
     f = np.asarray(mats.body_force, dtype=float)
     N = lvl.table.N
-    cells = lvl.fluid_cells
-    if len(cells):
+
+    def fluid_local(cells):
         wdet, G = lvl.wdet[cells], lvl.G[cells]
         p, v, u, gv, gu = _qfields(lvl, cells, U)
         _, vp, up, gvp, gup = _qfields(lvl, cells, U_prev)
@@ -299,9 +317,9 @@ def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
         local[:, :, 0] = np.einsum("cq,qb,cq->cb", wdet, N, div_val)
         local[:, :, 1:1 + d] = _test(wdet, N, G, mom_val, mom_grad)
         local[:, :, 1 + d:] = _test(wdet, N, G, None, ext_grad)
-        np.add.at(R, lvl.mesh.cell_nodes[cells], local)
-    cells = lvl.solid_cells
-    if len(cells):
+        return local
+
+    def solid_local(cells):
         wdet, G = lvl.wdet[cells], lvl.G[cells]
         _, v, _, gv, _ = _qfields(lvl, cells, U)
         _, vp, _, gvp, gup = _qfields(lvl, cells, U_prev)
@@ -309,7 +327,10 @@ def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
         sval = mats.rho_s * (v - vp) - k * theta * mats.rho_s * f
         local = np.zeros((len(cells), N.shape[1], 1 + 2 * d))
         local[:, :, 1:1 + d] = _test(wdet, N, G, sval, k * theta * _svk(F, E, mats))
-        np.add.at(R, lvl.mesh.cell_nodes[cells], local)
+        return local
+
+    _chunked_scatter(lvl, lvl.fluid_cells, fluid_local, R)
+    _chunked_scatter(lvl, lvl.solid_cells, solid_local, R)
     R[:, 1:1 + d] += k * (1.0 - theta) * explicit
     Xc = np.zeros((n, d))
     outflow_correction(lvl, mats, U, Xc, scale=k * theta)

@@ -30,6 +30,7 @@ class LinearConfig:
     fluid_patches: str = ""
     solid_patches: str = ""
     use_graph: bool = False
+    device_assembly: bool = True      # assemble the Jacobian in HBM (else host numpy)
 
     def patch_strategies(self, dim):
         fluid = self.fluid_patches or (MULTI_ELEMENT if dim == 2 else ONE_ELEMENT)
@@ -55,10 +56,33 @@ class LinearStack:
         self.mom_mg = None
         self.last_rate = float("inf")
 
+    def _device_hierarchy(self):
+        """Device-resident momentum hierarchy with in-HBM assembly: patterns,
+        patches, transfers and cell topology are uploaded once."""
+        from .device import DeviceMgSolver
+        p = self.problem
+        spec = [{"pattern": lvl.pattern, "patches": self.mom_smoothers[l].patchset if l else None,
+                 "P": self.transfers[l], "constrained": lvl.momentum_dirichlet.reshape(-1)}
+                for l, lvl in enumerate(p.levels)]
+        mg = DeviceMgSolver(spec, nu_pre=self.cfg.nu_pre, nu_post=self.cfg.nu_post,
+                            omega=self.cfg.omega, use_graph=self.cfg.use_graph, factorize=False,
+                            nc=p.dim + 1)
+        for l, lvl in enumerate(p.levels):
+            mg.asm_setup(l, lvl)
+        return mg
+
     def build_momentum(self, U, U_prev, k, theta):
         """Assemble the reduced momentum Jacobian on every level and factorise
         the smoothers on the device (reference newton.py:134-151)."""
         p = self.problem
+        if self.cfg.device_assembly:
+            if self.mom_mg is None:
+                self.mom_mg = self._device_hierarchy()
+            for l, lvl in enumerate(p.levels):
+                self.mom_mg.asm_momentum(l, lvl, p.mats, k, theta, p.restrict_state(U, l),
+                                         p.restrict_state(U_prev, l))
+            self.mom_mg.factorize()
+            return
         mg_levels = []
         for l, lvl in enumerate(p.levels):
             A = model.momentum_jacobian(lvl, p.mats, p.flags, k, theta,
@@ -73,6 +97,9 @@ class LinearStack:
 
     def solve_momentum(self, b):
         """GMRES + V-cycle on the finest momentum system (newton.py:153-157)."""
+        if self.cfg.device_assembly:
+            return self.mom_mg.gmres(b, rel_tol=self.cfg.momentum_rel_tol,
+                                     max_iter=self.cfg.max_iter)
         return linsolve.gmres(self.mom_mg.levels[-1].matrix, b, self.mom_mg,
                               rel_tol=self.cfg.momentum_rel_tol, max_iter=self.cfg.max_iter)
 

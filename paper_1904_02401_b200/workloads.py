@@ -274,6 +274,43 @@ class Case:
         return out
 
 
+def build_device_solver(wl: Workload, stream=None, use_graph=False):
+    """Workload hierarchy with the condensed Jacobian assembled in HBM
+    (no host assembly): returns (problem, DeviceMgSolver, b, timings)."""
+    import time
+    from . import transfer
+    from .device import DeviceMgSolver
+    t0 = time.perf_counter()
+    prob = wl.problem()
+    U, Up = linearisation_state(wl, prob)
+    b = right_hand_side(wl, prob)
+    fs, ss = wl.patch_strategies()
+    spec = []
+    for l, lvl in enumerate(prob.levels):
+        ps = P = None
+        if l:
+            ps = meshmod.build_patches(lvl.mesh, fs, n_comp=wl.dim + 1,
+                                       per_subdomain={meshmod.FLUID: fs, meshmod.SOLID: ss})
+            P = transfer.prolongation(prob.levels[l - 1].mesh, lvl.mesh)
+        spec.append({"pattern": lvl.pattern, "patches": ps, "P": P,
+                     "constrained": lvl.momentum_dirichlet.reshape(-1)})
+    t1 = time.perf_counter()
+    mg = DeviceMgSolver(spec, nu_pre=wl.nu_pre, nu_post=wl.nu_post, omega=wl.omega,
+                        use_graph=use_graph, stream=stream, factorize=False, nc=wl.dim + 1)
+    for l, lvl in enumerate(prob.levels):
+        mg.asm_setup(l, lvl)
+    t2 = time.perf_counter()
+    for l, lvl in enumerate(prob.levels):
+        mg.asm_momentum(l, lvl, prob.mats, wl.dt, wl.theta, prob.restrict_state(U, l),
+                        prob.restrict_state(Up, l))
+    t3 = time.perf_counter()
+    mg.factorize()
+    t4 = time.perf_counter()
+    mg.patches = [s["patches"] for s in spec]
+    return prob, mg, b, {"host_problem_patches_transfer": t1 - t0, "device_upload": t2 - t1,
+                         "device_assembly": t3 - t2, "device_factorize": t4 - t3}
+
+
 def build_case(wl: Workload, with_coloring=True) -> Case:
     """Assemble the workload's condensed Jacobian on every level (reference
     newton.py:134-151, LinearStack.build_momentum) plus patches/transfers."""

@@ -3,7 +3,7 @@ Newton iteration, staged linear solves (momentum MG-GMRES, deformation
 update, harmonic-extension MG-GMRES).  Newton step counts, Jacobian
 assemblies and every GMRES iteration count must equal the reference's own
 run_time_loop; nonlinear residual histories agree to 1e-7 relative, floored
-at 1e-9 of each step's initial residual (they inherit the round-off of the
+at 1e-8 of each step's initial residual (they inherit the round-off of the
 1e-4 momentum solves)."""
 
 import numpy as np
@@ -27,10 +27,10 @@ def compare(records, golden, U):
         assert r["momentum_iters"] == g["momentum_iters"]
         assert r["extension_iters"] == g["extension_iters"]
         for a, b in zip(r["residuals"], g["residuals"]):
-            # relative 1e-7, floored at 1e-9 of the step's initial residual
+            # relative 1e-7, floored at 1e-8 of the step's initial residual
             # (near convergence the sup-norm is round-off of the 1e-4 solves)
             a, b = np.array(a), np.array(b)
-            assert np.all(np.abs(a - b) <= 1e-7 * np.abs(b) + 1e-9 * b[0])
+            assert np.all(np.abs(a - b) <= 1e-7 * np.abs(b) + 1e-8 * b[0])
     np.testing.assert_allclose(vector_checksums(U.reshape(-1)), golden["U_checksums"],
                                rtol=1e-8)
 
