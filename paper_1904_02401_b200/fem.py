@@ -97,7 +97,9 @@ class ShapeTable:
 
 def _jacobian(dN, X):
     """J[c,q,i,j] = sum_b X[c,b,i] dN[q,b,j]."""
-    return np.einsum("cbi,qbj->cqij", X, dN, optimize=True)
+    # plain (unoptimised) einsum: same summation order as the reference
+    # (fem.py:97), so the geometry is bitwise identical
+    return np.einsum("qbj,cbi->cqij", dN, X)
 
 
 def cell_geometry(mesh, table, weights, cells=None, chunk=16384):
@@ -114,7 +116,7 @@ def cell_geometry(mesh, table, weights, cells=None, chunk=16384):
         if np.any(det <= 0):
             raise GeometryError("non-positive cell map determinant")
         Jinv = np.linalg.inv(J)
-        G[s:s + chunk] = np.einsum("qbj,cqji->cqbi", table.dN, Jinv, optimize=True)
+        G[s:s + chunk] = np.einsum("qbj,cqji->cqbi", table.dN, Jinv)
         wdet[s:s + chunk] = det * weights[None, :]
     return G, wdet
 
@@ -163,7 +165,7 @@ class FacetQuadrature:
             J = _jacobian(table.dN, X)
             det = np.linalg.det(J)
             Jinv = np.linalg.inv(J)
-            G = np.einsum("qbj,cqji->cqbi", table.dN, Jinv, optimize=True)
+            G = np.einsum("qbj,cqji->cqbi", table.dN, Jinv)
             cof = det[..., None] * np.einsum("cqji,j->cqi", Jinv, nref)
             mag = np.linalg.norm(cof, axis=-1)
             parts["N"].append(np.broadcast_to(table.N, (len(sel),) + table.N.shape))

@@ -50,11 +50,13 @@ class MaterialParams:
 
 def _fields(G, N, Uc, d):
     """Values and gradients of v (comps 1..d) and u (comps d+1..2d) at qpoints."""
-    v = np.matmul(N[None], Uc[:, :, 1:1 + d])
-    u = np.matmul(N[None], Uc[:, :, 1 + d:])
-    GT = np.swapaxes(G, 2, 3)                                  # (c, q, j, b)
-    gv = np.swapaxes(np.matmul(GT, Uc[:, None, :, 1:1 + d]), 2, 3)
-    gu = np.swapaxes(np.matmul(GT, Uc[:, None, :, 1 + d:]), 2, 3)
+    # same contraction order as the reference (model.py:119-131): the
+    # Newton/GMRES iteration counts of the time loop are sensitive to the
+    # last bit of the residual near the 1e-4 linear tolerance
+    v = np.einsum("qb,cbi->cqi", N, Uc[:, :, 1:1 + d])
+    u = np.einsum("qb,cbi->cqi", N, Uc[:, :, 1 + d:])
+    gv = np.einsum("cqbj,cbi->cqij", G, Uc[:, :, 1:1 + d])
+    gu = np.einsum("cqbj,cbi->cqij", G, Uc[:, :, 1 + d:])
     return v, u, gv, gu
 
 
@@ -196,10 +198,9 @@ def _test(wdet, N, G, val, grad):
     """sum_q w (N_b val_i + G_b . grad_i) -> (c, b, i) (model.py:147-154)."""
     out = 0.0
     if val is not None:
-        out = out + np.matmul(N.T[None], wdet[:, :, None] * val)
+        out = out + np.einsum("cq,qb,cqi->cbi", wdet, N, val)
     if grad is not None:
-        wg = np.swapaxes(grad * wdet[:, :, None, None], 2, 3)      # (c, q, j, i)
-        out = out + np.matmul(G, wg).sum(axis=1)
+        out = out + np.einsum("cq,cqbj,cqij->cbi", wdet, G, grad)
     return out
 
 
@@ -207,9 +208,9 @@ def _qfields(lvl, cells, U):
     d = lvl.dim
     Uc = U[lvl.mesh.cell_nodes[cells]]
     N = lvl.table.N
-    p = N @ Uc[:, :, 0].T
+    p = np.einsum("qb,cb->cq", N, Uc[:, :, 0])
     v, u, gv, gu = _fields(lvl.G[cells], N, Uc, d)
-    return p.T, v, u, gv, gu
+    return p, v, u, gv, gu
 
 
 def outflow_correction(lvl, mats, U, X, scale=1.0):
@@ -304,7 +305,7 @@ def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
         mom_grad = (k * theta * mats.mu_f * J[..., None, None]
                     * (gvFi + np.swapaxes(gvFi, -1, -2)) @ FiT
                     - k * (J * p)[..., None, None] * FiT)
-        div_val = k * J * np.einsum("cqij,cqji->cq", gv, Fi)
+        div_val = k * (J * np.einsum("cqij,cqji->cq", gv, Fi))
         if flags.extension_model == "harmonic":
             ext_grad = k * gu
         else:
