@@ -307,6 +307,7 @@ def build_device_solver(wl: Workload, stream=None, use_graph=False):
     mg.factorize()
     t4 = time.perf_counter()
     mg.patches = [s["patches"] for s in spec]
+    mg.prolongations = [s["P"] for s in spec]
     return prob, mg, b, {"host_problem_patches_transfer": t1 - t0, "device_upload": t2 - t1,
                          "device_assembly": t3 - t2, "device_factorize": t4 - t3}
 
