@@ -113,6 +113,15 @@ int alefsi_mg_asm_tables(alefsi_mg h, int32_t dim, int32_t nq, const double* N, 
 int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, const double* U,
                            const double* U_prev, int64_t n_extra, const int64_t* extra_slots,
                            const double* extra_vals);
+/* Cell parts of the theta-step residual (which = 0, model.theta_residual,
+ * reference model.py:208-275, out (n_nodes, 1+2dim)) or of the explicit
+ * previous-state forces (which = 1, model.explicit_forces, model.py:159-185,
+ * out (n_nodes, dim)) on the device; params = {rho_f, mu_f, rho_s, mu_s,
+ * lam_s, k, theta, f0, f1, f2, ext_model (0 harmonic, 1 linear elasticity),
+ * ext_mu, ext_lam, ext_volume_scaling}.  Host arrays; U may be NULL for
+ * which = 1. */
+int alefsi_mg_asm_residual(alefsi_mg h, int32_t level, const double* params, const double* U,
+                           const double* U_prev, int32_t which, double* out);
 /* Copy a level's operator data (blocks, pp entries) to host memory. */
 int alefsi_mg_get_matrix(alefsi_mg h, int32_t level, double* data, double* pp_data);
 

@@ -336,6 +336,262 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
   }
 }
 
+// Cell parts of the theta-step residual (reference model.py:208-275) and of
+// the explicit previous-state forces (model.py:159-185).  KIND 0: fluid
+// residual rows (p, v, u), 1: solid residual rows (v), 2: fluid explicit
+// forces, 3: solid explicit forces.  out: (n_nodes, 1+2d) for KIND 0/1,
+// (n_nodes, d) for KIND 2/3; cells of one colour, no atomics.
+template <int D, int KIND>
+__global__ void __launch_bounds__(128) residual_cells_kernel(ResArgs a, const int32_t* cells,
+                                                             double* out) {
+  constexpr int NB = (D == 3) ? 27 : 9, NQ = NB, NF = 1 + 2 * D;
+  constexpr int NO = (KIND <= 1) ? NF : D;            // output fields per node
+  __shared__ double X[NB][D], U[NB][NF], Up[NB][NF];
+  __shared__ double G[NQ][NB][D];
+  __shared__ double val[NQ][NO];                        // tested with N_b
+  __shared__ double grd[NQ][NO][D];                     // tested with grad N_b
+  __shared__ double wq[NQ];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  const int64_t cell = cells[blockIdx.x];
+  const int32_t* cn = a.cell_nodes + cell * NB;
+  if (tid == 0) bad = 0;
+  for (int t = tid; t < NB * D; t += blockDim.x) X[t / D][t % D] = a.coords[(int64_t)cn[t / D] * D + t % D];
+  for (int t = tid; t < NB * NF; t += blockDim.x) {
+    const int b = t / NF, f = t - b * NF;
+    U[b][f] = a.U[(int64_t)cn[b] * NF + f];
+    Up[b][f] = a.Up[(int64_t)cn[b] * NF + f];
+  }
+  __syncthreads();
+  if (tid < NQ) {
+    const int q = tid;
+    double J[D][D], Ji[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double acc = 0.0;
+        for (int b = 0; b < NB; ++b) acc += cdN[(q * NB + b) * 3 + j] * X[b][i];
+        J[i][j] = acc;
+      }
+    const double dt = det<D>(J);
+    if (!(dt > 0.0)) bad = 1;
+    inv<D>(J, Ji, dt);
+    wq[q] = dt * cW[q];
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc += cdN[(q * NB + b) * 3 + j] * Ji[j][i];
+        G[q][b][i] = acc;
+      }
+  }
+  __syncthreads();
+  double vol = 0.0;
+  if (KIND == 0 && a.ext_model == 1 && a.ext_volume_scaling)
+    for (int q = 0; q < NQ; ++q) vol += wq[q];
+  if (tid < NQ) {
+    const int q = tid;
+    double p = 0.0, v[D], u[D], vp[D], up[D], gv[D][D], gu[D][D], gvp[D][D], gup[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      v[i] = u[i] = vp[i] = up[i] = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) gv[i][j] = gu[i][j] = gvp[i][j] = gup[i][j] = 0.0;
+    }
+    for (int b = 0; b < NB; ++b) {
+      const double nb = cN[q * NB + b];
+      p += nb * U[b][0];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        v[i] += nb * U[b][1 + i];
+        u[i] += nb * U[b][1 + D + i];
+        vp[i] += nb * Up[b][1 + i];
+        up[i] += nb * Up[b][1 + D + i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double g = G[q][b][j];
+          gv[i][j] += g * U[b][1 + i];
+          gu[i][j] += g * U[b][1 + D + i];
+          gvp[i][j] += g * Up[b][1 + i];
+          gup[i][j] += g * Up[b][1 + D + i];
+        }
+      }
+    }
+    const double kt = a.k * a.theta;
+    if constexpr (KIND == 0 || KIND == 2) {
+      // KIND 2 evaluates the previous state: use (vp, gvp, gup) as (v, gv, gu)
+      const double (&V)[D] = KIND == 0 ? v : vp;
+      const double (&GV)[D][D] = KIND == 0 ? gv : gvp;
+      const double (&GU)[D][D] = KIND == 0 ? gu : gup;
+      double F[D][D], Fi[D][D], gvFi[D][D];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) F[i][j] = GU[i][j] + (i == j ? 1.0 : 0.0);
+      const double Jd = det<D>(F);
+      if (!(Jd > 0.0)) bad = 2;
+      inv<D>(F, Fi, Jd);
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double g = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) g += GV[i][m] * Fi[m][j];
+          gvFi[i][j] = g;
+        }
+      double conv[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        double c = 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) c += gvFi[i][j] * V[j];
+        conv[i] = c - a.f[i];
+      }
+      // symmetric viscous stress (gvFi + gvFi^T) F^-T
+      double visc[D][D];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) s += (gvFi[i][m] + gvFi[m][i]) * Fi[j][m];
+          visc[i][j] = s;
+        }
+      if constexpr (KIND == 2) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          val[q][i] = a.rho_f * Jd * conv[i];
+#pragma unroll
+          for (int j = 0; j < D; ++j) grd[q][i][j] = a.mu_f * Jd * visc[i][j];
+        }
+      } else {
+        double Fp[D][D], Fb[D][D], Fbi[D][D];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            Fp[i][j] = gup[i][j] + (i == j ? 1.0 : 0.0);
+            Fb[i][j] = 0.5 * (F[i][j] + Fp[i][j]);
+          }
+        const double Jp = det<D>(Fp);
+        if (!(Jp > 0.0)) bad = 2;
+        inv<D>(Fb, Fbi, det<D>(Fb));
+        const double Jbar = 0.5 * (Jd + Jp);
+        double w[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) s += Fbi[i][j] * (u[j] - up[j]);
+          w[i] = s;
+        }
+        double trgvFi = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) trgvFi += gvFi[i][i];
+        val[q][0] = a.k * Jd * trgvFi;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          double vbw = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) vbw += 0.5 * (gv[i][j] + gvp[i][j]) * w[j];
+          val[q][1 + i] = a.rho_f * Jbar * (v[i] - vp[i]) - a.rho_f * Jbar * vbw +
+                          kt * a.rho_f * Jd * conv[i];
+          val[q][1 + D + i] = 0.0;
+          grd[q][0][i] = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) {
+            grd[q][1 + i][j] = kt * a.mu_f * Jd * visc[i][j] - a.k * Jd * p * Fi[j][i];
+            double e;
+            if (a.ext_model == 0) {
+              e = a.k * gu[i][j];
+            } else {
+              const double eps = 0.5 * (gu[i][j] + gu[j][i]);
+              double tr = 0.0;
+#pragma unroll
+              for (int m = 0; m < D; ++m) tr += gu[m][m];
+              e = a.k * (2.0 * a.ext_mu * eps + (i == j ? a.ext_lam * tr : 0.0));
+              if (a.ext_volume_scaling) e /= vol;
+            }
+            grd[q][1 + D + i][j] = e;
+          }
+        }
+      }
+    } else {
+      // solid: KIND 1 condensed gradient at the new velocity, KIND 3 the
+      // previous deformation gradient
+      double F[D][D], E[D][D], Sig[D][D];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+          F[i][j] = (KIND == 1 ? gup[i][j] + kt * gv[i][j] + a.k * (1.0 - a.theta) * gvp[i][j]
+                               : gup[i][j]) + (i == j ? 1.0 : 0.0);
+      if (!(det<D>(F) > 0.0)) bad = 3;
+      double tr = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double e = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) e += F[m][i] * F[m][j];
+          E[i][j] = 0.5 * (e - (i == j ? 1.0 : 0.0));
+        }
+#pragma unroll
+      for (int i = 0; i < D; ++i) tr += E[i][i];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) Sig[i][j] = 2.0 * a.mu_s * E[i][j] + (i == j ? a.lam_s * tr : 0.0);
+      const double sc = KIND == 1 ? kt : 1.0;
+      if constexpr (KIND == 1) {
+        val[q][0] = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          val[q][1 + D + i] = 0.0;
+          grd[q][0][i] = 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) grd[q][1 + D + i][j] = 0.0;
+        }
+      }
+      constexpr int OFF = KIND == 1 ? 1 : 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        val[q][OFF + i] = KIND == 1 ? a.rho_s * (v[i] - vp[i]) - kt * a.rho_s * a.f[i]
+                                    : -a.rho_s * a.f[i];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          double P = 0.0;
+#pragma unroll
+          for (int m = 0; m < D; ++m) P += F[i][m] * Sig[m][j];
+          grd[q][OFF + i][j] = sc * P;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (bad) {
+    if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(a.status), 0ull,
+                            (unsigned long long)(cell + 1));
+    return;
+  }
+  for (int t = tid; t < NB * NO; t += blockDim.x) {
+    const int b = t / NO, f = t - b * NO;
+    double acc = 0.0;
+    for (int q = 0; q < NQ; ++q) {
+      double s = cN[q * NB + b] * val[q][f];
+#pragma unroll
+      for (int j = 0; j < D; ++j) s += G[q][b][j] * grd[q][f][j];
+      acc += wq[q] * s;
+    }
+    out[(int64_t)cn[b] * NO + f] += acc;
+  }
+}
+
 // data[slot] += vals (unique slots; host-reduced facet contributions)
 __global__ void add_blocks_kernel(double* data, int bs, int64_t n, const int64_t* slots,
                                   const double* vals) {
@@ -403,6 +659,23 @@ void launch_assemble_cells(const AsmArgs& a, int dim, int kind, const int32_t* c
   } else {
     cudaFuncSetAttribute(assemble_cells_kernel<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     assemble_cells_kernel<2, 1><<<(unsigned)n_cells, 128, smem, s>>>(a, cells, n_cells);
+  }
+}
+
+void launch_residual_cells(const ResArgs& a, int dim, int kind, const int32_t* cells,
+                           int64_t n_cells, double* out, cudaStream_t s) {
+  if (n_cells == 0) return;
+  const unsigned g = (unsigned)n_cells;
+  if (dim == 3) {
+    if (kind == 0) residual_cells_kernel<3, 0><<<g, 128, 0, s>>>(a, cells, out);
+    else if (kind == 1) residual_cells_kernel<3, 1><<<g, 128, 0, s>>>(a, cells, out);
+    else if (kind == 2) residual_cells_kernel<3, 2><<<g, 128, 0, s>>>(a, cells, out);
+    else residual_cells_kernel<3, 3><<<g, 128, 0, s>>>(a, cells, out);
+  } else {
+    if (kind == 0) residual_cells_kernel<2, 0><<<g, 128, 0, s>>>(a, cells, out);
+    else if (kind == 1) residual_cells_kernel<2, 1><<<g, 128, 0, s>>>(a, cells, out);
+    else if (kind == 2) residual_cells_kernel<2, 2><<<g, 128, 0, s>>>(a, cells, out);
+    else residual_cells_kernel<2, 3><<<g, 128, 0, s>>>(a, cells, out);
   }
 }
 

@@ -17,6 +17,24 @@ struct AsmArgs {
   double rho_f = 0, mu_f = 0, rho_s = 0, mu_s = 0, lam_s = 0, k = 0, theta = 0;
 };
 
+struct ResArgs {
+  const int32_t* cell_nodes = nullptr;
+  const double* coords = nullptr;
+  const double* U = nullptr;
+  const double* Up = nullptr;
+  int64_t* status = nullptr;
+  double rho_f = 0, mu_f = 0, rho_s = 0, mu_s = 0, lam_s = 0, k = 0, theta = 0;
+  double f[3] = {0, 0, 0};
+  int ext_model = 0;          // 0 harmonic, 1 linear elasticity
+  double ext_mu = 1, ext_lam = 0;
+  int ext_volume_scaling = 0;
+};
+
+// cell contributions of the theta residual (kind 0 fluid, 1 solid) or of the
+// explicit previous-state forces (kind 2 fluid, 3 solid), added into out
+void launch_residual_cells(const ResArgs& a, int dim, int kind, const int32_t* cells,
+                           int64_t n_cells, double* out, cudaStream_t s);
+
 // Q2 tables at the Gauss points: N (nq, nb), dN (nq, nb, dim), weights (nq)
 void set_assembly_tables(const double* N, const double* dN, const double* w, int nq, int nb,
                          int dim);

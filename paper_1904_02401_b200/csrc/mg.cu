@@ -130,7 +130,7 @@ struct Level {
   bool has_asm = false;
   int dim = 0;
   DevBuf<int32_t> asm_cell_nodes, asm_group_cells;
-  DevBuf<double> asm_coords, asm_U, asm_Up;
+  DevBuf<double> asm_coords, asm_U, asm_Up, res_out;
   std::vector<int64_t> asm_group_ptr;
   std::vector<int> asm_group_kind;
   int64_t n_lps = 0;
@@ -818,6 +818,65 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
                                          std::to_string(st - 1));
   m->factorized = false;
   m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+// params = rho_f, mu_f, rho_s, mu_s, lam_s, k, theta, f0, f1, f2, ext_model
+// (0 harmonic / 1 linear elasticity), ext_mu, ext_lam, ext_volume_scaling.
+// which = 0: cell parts of the theta residual -> out (n_nodes, 1+2d);
+// which = 1: cell parts of the explicit forces of U_prev -> out (n_nodes, d).
+// U, U_prev, out are host arrays.
+int alefsi_mg_asm_residual(alefsi_mg h, int32_t level, const double* params, const double* U,
+                           const double* Up, int32_t which, double* out) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (!L.has_asm) return fail(ALEFSI_ERR_STATE, "asm_setup missing");
+  const int d = L.dim, nf = 1 + 2 * d;
+  const int no = which == 0 ? nf : d;
+  cudaStream_t s = m->stream;
+  if (U) CKAPI(cudaMemcpyAsync(L.asm_U.p, U, sizeof(double) * L.n_nodes * nf, cudaMemcpyHostToDevice, s));
+  CKAPI(cudaMemcpyAsync(L.asm_Up.p, Up, sizeof(double) * L.n_nodes * nf, cudaMemcpyHostToDevice, s));
+  if (L.res_out.n != (size_t)L.n_nodes * nf) CKAPI(L.res_out.alloc((size_t)L.n_nodes * nf));
+  CKAPI(cudaMemsetAsync(L.res_out.p, 0, sizeof(double) * L.n_nodes * no, s));
+  CKAPI(cudaMemsetAsync(m->status.p, 0, sizeof(int64_t), s));
+  alefsi::ResArgs a;
+  a.cell_nodes = L.asm_cell_nodes.p;
+  a.coords = L.asm_coords.p;
+  a.U = L.asm_U.p;
+  a.Up = L.asm_Up.p;
+  a.status = m->status.p;
+  a.rho_f = params[0];
+  a.mu_f = params[1];
+  a.rho_s = params[2];
+  a.mu_s = params[3];
+  a.lam_s = params[4];
+  a.k = params[5];
+  a.theta = params[6];
+  a.f[0] = params[7];
+  a.f[1] = params[8];
+  a.f[2] = params[9];
+  a.ext_model = (int)params[10];
+  a.ext_mu = params[11];
+  a.ext_lam = params[12];
+  a.ext_volume_scaling = (int)params[13];
+  for (size_t g = 0; g + 1 < L.asm_group_ptr.size(); ++g) {
+    const int64_t b = L.asm_group_ptr[g], e = L.asm_group_ptr[g + 1];
+    const int kind = L.asm_group_kind[g] + (which == 1 ? 2 : 0);
+    alefsi::launch_residual_cells(a, d, kind, L.asm_group_cells.p + b, e - b, L.res_out.p, s);
+    ++m->kernel_launches;
+  }
+  CKAPI(cudaGetLastError());
+  CKAPI(cudaMemcpyAsync(out, L.res_out.p, sizeof(double) * L.n_nodes * no, cudaMemcpyDeviceToHost, s));
+  int64_t st = 0;
+  CKAPI(cudaMemcpyAsync(&st, m->status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CKAPI(cudaStreamSynchronize(s));
+  if (st != 0)
+    return fail(ALEFSI_ERR_SINGULAR, "inverted element in device residual: cell " +
+                                         std::to_string(st - 1));
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }

@@ -299,6 +299,20 @@ class DeviceMgSolver:
                   np.ascontiguousarray(slots, dtype=np.int64),
                   np.ascontiguousarray(vals, dtype=np.float64))
 
+    def asm_residual(self, level, lvl, mats, flags, k, theta, U, U_prev, which=0):
+        """Cell parts of the theta residual (which=0) or of the explicit
+        previous-state forces (which=1) evaluated on the device."""
+        d = lvl.dim
+        f = list(mats.body_force) + [0.0] * (3 - len(mats.body_force))
+        params = np.array([mats.rho_f, mats.mu_f, mats.rho_s, mats.mu_s, mats.lam_s, k, theta,
+                           f[0], f[1], f[2], 0.0 if flags.extension_model == "harmonic" else 1.0,
+                           flags.ext_mu, flags.ext_lam, 1.0 if flags.ext_volume_scaling else 0.0])
+        out = np.zeros((lvl.n_nodes, 1 + 2 * d if which == 0 else d))
+        _lib.call("alefsi_mg_asm_residual", self._h, level, params,
+                  None if U is None else np.ascontiguousarray(U, dtype=np.float64),
+                  np.ascontiguousarray(U_prev, dtype=np.float64), which, out)
+        return out
+
     def matrix_data(self, level, pattern):
         data = np.empty((pattern.nnzb, self.nc, self.nc))
         pp = np.empty(pattern.nnz_pp)

@@ -258,11 +258,23 @@ def explicit_forces(lvl, mats, flags, U_prev):
     return X
 
 
-def theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit=None):
+def theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit=None, device=None):
     """Residual of one theta step with constrained rows zeroed
-    (reference model.py:208-292).  Returns (R, explicit)."""
+    (reference model.py:208-292).  Returns (R, explicit).
+
+    ``device = (DeviceMgSolver, level)`` evaluates the cell integrals (the
+    bulk of the work) on the GPU; facet, LPS, mass-relation and masking terms
+    stay on the host."""
     with fem.single_blas():
-        return _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit)
+        if device is None:
+            return _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit)
+        mg, level = device
+        d = lvl.dim
+        if explicit is None:
+            explicit = mg.asm_residual(level, lvl, mats, flags, k, theta, None, U_prev, which=1)
+            outflow_correction(lvl, mats, U_prev, explicit)
+        R = mg.asm_residual(level, lvl, mats, flags, k, theta, U, U_prev, which=0)
+        return _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R), explicit
 
 
 def _chunked_scatter(lvl, cells, fn, out, chunk=1024):
@@ -332,6 +344,14 @@ def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
 
     _chunked_scatter(lvl, lvl.fluid_cells, fluid_local, R)
     _chunked_scatter(lvl, lvl.solid_cells, solid_local, R)
+    return _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R), explicit
+
+
+def _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R):
+    """Explicit theta part, outflow correction, LPS, velocity-deformation
+    relation rows and constraint masking (reference model.py:277-292)."""
+    d = lvl.dim
+    n = lvl.n_nodes
     R[:, 1:1 + d] += k * (1.0 - theta) * explicit
     Xc = np.zeros((n, d))
     outflow_correction(lvl, mats, U, Xc, scale=k * theta)
@@ -342,7 +362,7 @@ def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
     rel = lvl.solid_mass_csr() @ deficit
     R[lvl.relation_nodes, 1 + d:] = rel[lvl.relation_nodes]
     R[lvl.residual_zero_mask] = 0.0
-    return R, explicit
+    return R
 
 
 def extension_operator(lvl, flags):

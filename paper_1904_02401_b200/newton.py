@@ -54,7 +54,17 @@ class LinearStack:
             ps, col = linsolve.build_momentum_patches(levels[l].mesh, d, fs, ss)
             self.mom_smoothers.append(linsolve.VankaSmoother(ps, col, lin_cfg.omega))
         self.mom_mg = None
+        self.assembled = False
         self.last_rate = float("inf")
+
+    def residual_device(self):
+        """(device hierarchy, finest level) for device residual evaluation,
+        or None with host assembly."""
+        if not self.cfg.device_assembly:
+            return None
+        if self.mom_mg is None:
+            self.mom_mg = self._device_hierarchy()
+        return self.mom_mg, len(self.problem.levels) - 1
 
     def _device_hierarchy(self):
         """Device-resident momentum hierarchy with in-HBM assembly: patterns,
@@ -75,6 +85,7 @@ class LinearStack:
         """Assemble the reduced momentum Jacobian on every level and factorise
         the smoothers on the device (reference newton.py:134-151)."""
         p = self.problem
+        self.assembled = True
         if self.cfg.device_assembly:
             if self.mom_mg is None:
                 self.mom_mg = self._device_hierarchy()
@@ -223,12 +234,14 @@ def newton_solve(problem, stack, U_guess, U_prev, k, theta, cfg: NewtonConfig):
     stats = NewtonStats()
     cache = [None]
 
+    dev = stack.residual_device() if hasattr(stack, "residual_device") else None
+
     def residual_of(Ut):
         Ut = Ut.copy()
         model.deformation_update(Ut, U_prev, k, theta, lvl.relation_nodes)
         t0 = time.perf_counter()
         R, cache[0] = model.theta_residual(lvl, problem.mats, problem.flags, k, theta, Ut,
-                                           U_prev, cache[0])
+                                           U_prev, cache[0], device=dev)
         stats.residual_time += time.perf_counter() - t0
         return (Ut, R), float(np.abs(R).max())
 
@@ -239,7 +252,8 @@ def newton_solve(problem, stack, U_guess, U_prev, k, theta, cfg: NewtonConfig):
         if stats.steps >= cfg.max_steps:
             raise StepFailure(f"Newton did not converge in {cfg.max_steps} steps "
                               f"(residual {res:.3e})", stats)
-        if stack.mom_mg is None or stack.last_rate > cfg.gamma:
+        if not getattr(stack, "assembled", stack.mom_mg is not None) or \
+                stack.last_rate > cfg.gamma:
             t0 = time.perf_counter()
             stack.build_momentum(U, U_prev, k, theta)
             stats.assemble_time += time.perf_counter() - t0

@@ -28,6 +28,26 @@ def test_device_assembly_matches_host(name):
 
 
 @pytest.mark.parametrize("name", ["2d_mini", "3d_tiny"])
+@pytest.mark.parametrize("ext", ["harmonic", "linear_elasticity"])
+def test_device_residual_matches_host(name, ext):
+    """Cell integrals of the theta residual and explicit forces on the device
+    vs the host mirror (bitwise-pinned to the reference)."""
+    from paper_1904_02401_b200 import model
+    wl = W.CONFIGS[name]
+    prob, mg, b, _ = W.build_device_solver(wl)
+    prob.flags.extension_model = ext
+    U, _ = W.linearisation_state(wl, prob)
+    Up = 0.5 * U + 1e-3 * np.random.default_rng(5).standard_normal(U.shape)
+    for l, lvl in enumerate(prob.levels):
+        n = lvl.n_nodes
+        R, ex = model.theta_residual(lvl, prob.mats, prob.flags, wl.dt, wl.theta, U[:n], Up[:n])
+        Rd, exd = model.theta_residual(lvl, prob.mats, prob.flags, wl.dt, wl.theta, U[:n],
+                                       Up[:n], device=(mg, l))
+        assert np.abs(ex - exd).max() <= 1e-13 * max(1.0, np.abs(ex).max())
+        assert np.abs(R - Rd).max() <= 1e-13 * max(1.0, np.abs(R).max())
+
+
+@pytest.mark.parametrize("name", ["2d_mini", "3d_tiny"])
 def test_device_assembled_solve_matches_reference(name):
     g, arr = load_golden(name)
     wl = W.CONFIGS[name]
