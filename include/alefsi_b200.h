@@ -58,6 +58,11 @@ int alefsi_scatter_add_blocks(int64_t n_nodes, const int64_t* indptr, const int3
                               int64_t n_elem, int32_t npe, const int64_t* elem_nodes, int32_t bs,
                               const double* local, double* data, int32_t skip_missing);
 
+/* slot_in_a[s] = slot of entry s of row-sorted pattern B in pattern A, or -1
+ * (splits the LPS macro pattern against the cell pattern; fem.py:79-90). */
+int alefsi_pattern_match(int64_t n_nodes, const int64_t* a_ptr, const int32_t* a_idx,
+                         const int64_t* b_ptr, const int32_t* b_idx, int64_t* slot_in_a);
+
 /* Greedy first-fit patch coloring; replaces color_patches
  * (reference mesh.py:522-556).  patch_size is the dof count per patch. */
 int alefsi_color_patches(int64_t n_patches, const int64_t* patch_ptr, const int64_t* patch_nodes,

@@ -121,22 +121,56 @@ int alefsi_scatter_add_blocks(int64_t n_nodes, const int64_t* indptr, const int3
                               int32_t bs, const double* local, double* data,
                               int32_t skip_missing) {
   ALEFSI_TRY_BEGIN
-  for (int64_t e = 0; e < n_elem; ++e) {
-    const int64_t* nd = elem_nodes + e * npe;
-    const double* loc = local + e * (int64_t)npe * npe * bs;
-    for (int a = 0; a < npe; ++a)
-      for (int b = 0; b < npe; ++b) {
-        int64_t slot = find_slot(indptr, indices, nd[a], nd[b]);
-        const double* src = loc + ((int64_t)a * npe + b) * bs;
-        if (slot < 0) {
-          if (skip_missing) continue;
-          return alefsi::fail(ALEFSI_ERR_ARG, "scatter_add_blocks: pair outside pattern");
+  // Parallel over block rows: every slot of row r is only touched by the
+  // elements containing r, visited in ascending element order, so each slot
+  // receives its contributions in exactly the sequential (np.add.at) order.
+  std::vector<int64_t> eptr(n_elem + 1);
+  for (int64_t e = 0; e <= n_elem; ++e) eptr[e] = e * npe;
+  if (!check_nodes(n_nodes, n_elem, eptr.data(), elem_nodes))
+    return alefsi::fail(ALEFSI_ERR_ARG, "scatter_add_blocks: element node out of range");
+  std::vector<int64_t> ptr, adj;
+  node_element_adjacency(n_nodes, n_elem, eptr.data(), elem_nodes, ptr, adj);
+  int missing = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(| : missing)
+  for (int64_t r = 0; r < n_nodes; ++r) {
+    for (int64_t s = ptr[r]; s < ptr[r + 1]; ++s) {
+      const int64_t e = adj[s];
+      const int64_t* nd = elem_nodes + e * npe;
+      const double* loc = local + e * (int64_t)npe * npe * bs;
+      for (int a = 0; a < npe; ++a) {
+        if (nd[a] != r) continue;
+        for (int b = 0; b < npe; ++b) {
+          const int64_t slot = find_slot(indptr, indices, r, nd[b]);
+          if (slot < 0) {
+            missing |= 1;
+            continue;
+          }
+          const double* src = loc + ((int64_t)a * npe + b) * bs;
+          double* dst = data + slot * bs;
+          for (int k = 0; k < bs; ++k) dst[k] += src[k];
         }
-        double* dst = data + slot * bs;
-        for (int k = 0; k < bs; ++k) dst[k] += src[k];
       }
+    }
   }
-  (void)n_nodes;
+  if (missing && !skip_missing)
+    return alefsi::fail(ALEFSI_ERR_ARG, "scatter_add_blocks: pair outside pattern");
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+// For every entry of pattern B (rows sorted): its slot in pattern A or -1.
+int alefsi_pattern_match(int64_t n_nodes, const int64_t* a_ptr, const int32_t* a_idx,
+                         const int64_t* b_ptr, const int32_t* b_idx, int64_t* slot_in_a) {
+  ALEFSI_TRY_BEGIN
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t r = 0; r < n_nodes; ++r) {
+    int64_t i = a_ptr[r];
+    const int64_t ie = a_ptr[r + 1];
+    for (int64_t s = b_ptr[r]; s < b_ptr[r + 1]; ++s) {
+      while (i < ie && a_idx[i] < b_idx[s]) ++i;
+      slot_in_a[s] = (i < ie && a_idx[i] == b_idx[s]) ? i : -1;
+    }
+  }
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }

@@ -102,22 +102,29 @@ def _jacobian(dN, X):
     return np.einsum("qbj,cbi->cqij", dN, X)
 
 
-def cell_geometry(mesh, table, weights, cells=None, chunk=16384):
+def cell_geometry(mesh, table, weights, cells=None, chunk=2048):
     """Physical basis gradients G (nc, nq, nb, d) and weights*det (nc, nq)."""
     conn = mesh.cell_nodes if cells is None else mesh.cell_nodes[cells]
     nc = len(conn)
     nq, nb, d = table.dN.shape
     G = np.empty((nc, nq, nb, d))
     wdet = np.empty((nc, nq))
-    for s in range(0, nc, chunk):
+    bad = []
+
+    def work(s):
         X = mesh.nodes[conn[s:s + chunk]]
         J = _jacobian(table.dN, X)
         det = np.linalg.det(J)
         if np.any(det <= 0):
-            raise GeometryError("non-positive cell map determinant")
+            bad.append(s)
+            return
         Jinv = np.linalg.inv(J)
         G[s:s + chunk] = np.einsum("qbj,cqji->cqbi", table.dN, Jinv)
         wdet[s:s + chunk] = det * weights[None, :]
+
+    parallel_chunks(work, range(0, nc, chunk))
+    if bad:
+        raise GeometryError("non-positive cell map determinant")
     return G, wdet
 
 
@@ -361,25 +368,31 @@ class SplitPattern:
 
 def build_split_pattern(n_nodes, cell_groups, macro_nodes):
     indptr, indices = pattern_from_elements(n_nodes, cell_groups)
-    rows = np.repeat(np.arange(n_nodes, dtype=np.int64), np.diff(indptr))
-    key = rows * n_nodes + indices
-    diag = np.searchsorted(key, np.arange(n_nodes, dtype=np.int64) * (n_nodes + 1))
+    diag = pattern_match(indptr, indices, np.arange(n_nodes + 1, dtype=np.int64),
+                         np.arange(n_nodes, dtype=np.int32))
     if len(macro_nodes):
         mptr, mind = pattern_from_elements(n_nodes, [macro_nodes])
     else:
         mptr, mind = np.zeros(n_nodes + 1, dtype=np.int64), np.zeros(0, dtype=np.int32)
-    mrows = np.repeat(np.arange(n_nodes, dtype=np.int64), np.diff(mptr))
-    mkey = mrows * n_nodes + mind
-    pos = np.searchsorted(key, mkey)
-    hit = (pos < len(key)) & (key[np.minimum(pos, len(key) - 1)] == mkey)
-    to_cell = np.where(hit, pos, -1).astype(np.int64)
-    extra = ~hit
+    to_cell = pattern_match(indptr, indices, mptr, mind)
+    extra = to_cell < 0
     pp_indices = mind[extra].astype(np.int32)
-    pp_indptr = np.concatenate([[0], np.cumsum(np.bincount(mrows[extra], minlength=n_nodes))])
-    to_pp = np.full(len(mkey), -1, dtype=np.int64)
-    to_pp[extra] = np.arange(int(extra.sum()))
+    cs = np.concatenate([[0], np.cumsum(extra, dtype=np.int64)])
+    pp_indptr = cs[mptr]
+    to_pp = np.full(len(mind), -1, dtype=np.int64)
+    to_pp[extra] = np.arange(int(cs[-1]))
     return SplitPattern(n_nodes, indptr, indices, pp_indptr.astype(np.int64), pp_indices,
                         mptr, mind, to_cell, to_pp, diag.astype(np.int64))
+
+
+def pattern_match(a_ptr, a_idx, b_ptr, b_idx):
+    """Slot in pattern A of every entry of pattern B (-1 if absent); native."""
+    out = np.empty(len(b_idx), dtype=np.int64)
+    _lib.call("alefsi_pattern_match", len(a_ptr) - 1,
+              np.ascontiguousarray(a_ptr, dtype=np.int64), np.ascontiguousarray(a_idx, dtype=np.int32),
+              np.ascontiguousarray(b_ptr, dtype=np.int64), np.ascontiguousarray(b_idx, dtype=np.int32),
+              out)
+    return out
 
 
 @dataclass
