@@ -68,40 +68,10 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
   const int sub = lane / NC;
   const int64_t beg = indptr[row], end = indptr[row + 1];
   double acc = 0.0;
-  int64_t blk0 = beg + sub;
-  if constexpr (NC % 2 == 0) {
-    // 4 iterations per trip with every load issued before the first FMA, so
-    // each lane keeps 4 index + 4 block-row + 4 x loads in flight
-    constexpr int U = 4, H = NC / 2;
-    if (sub < BPI) {
-      for (; blk0 + (U - 1) * BPI < end; blk0 += U * BPI) {
-        int64_t col[U];
-        double2 vv[U][H], xx[U][H];
-#pragma unroll
-        for (int u = 0; u < U; ++u) col[u] = __ldcs(indices + blk0 + u * BPI);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int c = 0; c < H; ++c)
-            vv[u][c] = __ldcs(reinterpret_cast<const double2*>(
-                                  data + (blk0 + u * BPI) * (NC * NC) + r * NC) + c);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int c = 0; c < H; ++c)
-            xx[u][c] = __ldg(reinterpret_cast<const double2*>(x + col[u] * NC) + c);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int c = 0; c < H; ++c) {
-            acc = fma(vv[u][c].x, xx[u][c].x, acc);
-            acc = fma(vv[u][c].y, xx[u][c].y, acc);
-          }
-      }
-    }
-  }
+  // (a 4-way manually unrolled variant measured 16% slower: the extra
+  // registers cost occupancy, and 64 warps/SM already cover the latency)
   if (sub < BPI) {
-    for (int64_t blk = blk0; blk < end; blk += BPI) {
+    for (int64_t blk = beg + sub; blk < end; blk += BPI) {
       const int64_t col = __ldcs(indices + blk);
       const double* v = data + blk * (NC * NC) + r * NC;
       const double* xv = x + col * NC;
