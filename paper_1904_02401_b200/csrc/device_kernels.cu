@@ -122,6 +122,57 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
   }
 }
 
+// Odd block size (NC = 3, 2D): a row's blocks are one contiguous run of
+// 9*nb doubles, streamed with fully coalesced 8-byte loads (lane l takes
+// elements l, l+32, ...); each lane keeps one partial sum per block row.
+template <int NC, int MODE>
+__global__ void __launch_bounds__(256) spmv_flat_kernel(int64_t n, const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ indices,
+                                                        const double* __restrict__ data,
+                                                        const int64_t* __restrict__ pp_ptr,
+                                                        const int32_t* __restrict__ pp_idx,
+                                                        const double* __restrict__ pp_val,
+                                                        const double* __restrict__ x,
+                                                        const double* __restrict__ b,
+                                                        double* __restrict__ y) {
+  constexpr int BS = NC * NC;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  const int64_t beg = indptr[row], end = indptr[row + 1];
+  const int64_t ne = (end - beg) * BS;
+  const double* rd = data + beg * BS;
+  double acc[NC];
+#pragma unroll
+  for (int r = 0; r < NC; ++r) acc[r] = 0.0;
+#pragma unroll 4
+  for (int64_t e = lane; e < ne; e += kWarp) {
+    const int64_t blk = e / BS;
+    const int w = (int)(e - blk * BS);
+    const int r = w / NC, c = w - r * NC;
+    const double v = __ldcs(rd + e) * __ldg(x + (int64_t)__ldg(indices + beg + blk) * NC + c);
+#pragma unroll
+    for (int rr = 0; rr < NC; ++rr)
+      if (rr == r) acc[rr] += v;
+  }
+  double accp = 0.0;
+  if (pp_ptr != nullptr) {
+    for (int64_t e = pp_ptr[row] + lane; e < pp_ptr[row + 1]; e += kWarp)
+      accp = fma(__ldcs(pp_val + e), __ldg(x + (int64_t)__ldcs(pp_idx + e) * NC), accp);
+  }
+  acc[0] += accp;
+#pragma unroll
+  for (int rr = 0; rr < NC; ++rr) acc[rr] = warp_sum(acc[rr]);
+  if (lane < NC) {
+    double v = acc[0];
+#pragma unroll
+    for (int rr = 1; rr < NC; ++rr)
+      if (lane == rr) v = acc[rr];
+    const int64_t o = row * NC + lane;
+    y[o] = MODE == 1 ? b[o] - v : v;
+  }
+}
+
 // --------------------------------------------------------------------------
 // Vanka apply: Y[p] = A_p^{-1} d[dofs_p].  Inverses are stored column-major
 // with an even column length LD, so thread t of a patch owns rows 2t, 2t+1
@@ -587,6 +638,15 @@ template <int NC>
 void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
                    cudaStream_t s) {
   const int grid = grid_for(A.n_nodes * 32, 256);
+  if constexpr (NC % 2 == 1) {
+    if (mode == 0)
+      spmv_flat_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+                                                   A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
+    else
+      spmv_flat_kernel<NC, 1><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+                                                   A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
+    return;
+  }
   if (mode == 0)
     spmv_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
                                             A.pp_indices, A.pp_data, x, b, y);
