@@ -171,6 +171,21 @@ def test_device_full_size_vs_reference_history(name):
     np.testing.assert_allclose(vector_checksums(x), g["x_checksums"], rtol=1e-9)
 
 
+@pytest.mark.parametrize("name", ["3d_large"])
+def test_device_full_size_vs_oracle_history(name):
+    """The headline 4.3M-dof solve against the CPU oracle's full-size run
+    (tests/golden/make_oracle_golden.py; the oracle is pinned to the
+    reference on every size the reference can run here)."""
+    if not os.path.exists(os.path.join(GOLDEN, f"{name}_oracle.json")):
+        pytest.skip("oracle golden file not generated")
+    g, _ = load_golden(f"{name}_oracle")
+    wl = W.CONFIGS[name]
+    s = solver_for(name)
+    x, st = s.gmres(get_case(name).b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    assert_history(st, g["residuals"], g["iterations"])
+    np.testing.assert_allclose(vector_checksums(x), g["x_checksums"], rtol=1e-9)
+
+
 def test_device_headline_size_properties():
     """3D 4.3M-dof workload (BASELINE config 3): size-independent checks —
     convergence with a monotone history, true residual, V-cycle linearity,
