@@ -180,15 +180,20 @@ __global__ void __launch_bounds__(256) spmv_flat_kernel(int64_t n, const int64_t
 // LD*8-byte run, read exactly once per sweep with evict-first loads.  The
 // patch defect is staged in shared memory and broadcast.
 // --------------------------------------------------------------------------
+template <int LD>
+struct ApplyShape {
+  static constexpr int TPP = ((LD / 2 + 31) / 32) * 32;   // threads per patch
+  static constexpr int BLK = TPP > 128 ? TPP : 128;       // CTA size
+  static constexpr int PPC = BLK / TPP;                   // patches per CTA
+};
+
 template <int NP, int LD, int NC>
-__global__ void __launch_bounds__(128) vanka_apply_kernel(int64_t n_patches,
-                                                          const int32_t* __restrict__ nodes,
-                                                          const double* __restrict__ inv,
-                                                          const double* __restrict__ d,
-                                                          double* __restrict__ Y) {
+__global__ void __launch_bounds__(ApplyShape<LD>::BLK) vanka_apply_kernel(
+    int64_t n_patches, const int32_t* __restrict__ nodes, const double* __restrict__ inv,
+    const double* __restrict__ d, double* __restrict__ Y) {
   constexpr int NPN = NP / NC;
-  constexpr int TPP = ((LD / 2 + 31) / 32) * 32;  // threads per patch
-  constexpr int PPC = 128 / TPP;                  // patches per CTA
+  constexpr int TPP = ApplyShape<LD>::TPP;
+  constexpr int PPC = ApplyShape<LD>::PPC;
   static_assert(PPC >= 1, "patch too large for one CTA");
   __shared__ double ds[PPC][LD];
   const int sub = threadIdx.x / TPP, t = threadIdx.x % TPP;
@@ -381,6 +386,135 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
   if (ld > NP)
     for (int col = tid; col < NP; col += NT)
       for (int r = NP; r < ld; ++r) out[(int64_t)col * ld + r] = 0.0;
+}
+
+// --------------------------------------------------------------------------
+// Large patches (2x2x2-cell macros in 3D: 500 x 500): batched Gauss-Jordan
+// in global memory, one pivot step per launch pair over all patches of the
+// group, same implicit pivoting and output mapping as the register kernel.
+// --------------------------------------------------------------------------
+__global__ void big_gather_kernel(DevMatrix A, int np_, int npn, const int32_t* nodes,
+                                  double* M, int* used) {
+  const int64_t p = blockIdx.y;
+  const int32_t* pn = nodes + p * npn;
+  double* Mp = M + p * (int64_t)np_ * np_;
+  const int nc = A.nc;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)np_ * np_;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / np_), j = (int)(e - (int64_t)i * np_);
+    const int a = i / nc, ci = i - a * nc, b = j / nc, cj = j - b * nc;
+    const int64_t ra = pn[a];
+    const int32_t cb = pn[b];
+    int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
+    }
+    double v = 0.0;
+    if (lo < A.indptr[ra + 1] && A.indices[lo] == cb) {
+      v = A.data[lo * nc * nc + ci * nc + cj];
+    } else if (ci == 0 && cj == 0 && A.pp_indptr != nullptr) {
+      lo = A.pp_indptr[ra];
+      hi = A.pp_indptr[ra + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
+      }
+      if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) v = A.pp_data[lo];
+    }
+    Mp[e] = v;
+  }
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < np_; i += blockDim.x) used[p * np_ + i] = 0;
+}
+
+// pivot of step k for patch blockIdx.x: publish column k and the scaled row
+__global__ void __launch_bounds__(512) big_pivot_kernel(int np_, int k, double* M, int* used,
+                                                        int* perm, double* colk, double* prow,
+                                                        int64_t* status) {
+  __shared__ double sb[16];
+  __shared__ int si[16];
+  __shared__ int prs;
+  const int64_t p = blockIdx.x;
+  double* Mp = M + p * (int64_t)np_ * np_;
+  int* up = used + p * np_;
+  double best = -1.0;
+  int bi = np_;
+  for (int r = threadIdx.x; r < np_; r += blockDim.x) {
+    const double v = Mp[(int64_t)r * np_ + k];
+    colk[p * np_ + r] = v;
+    const double a = up[r] ? -1.0 : fabs(v);
+    if (a > best) { best = a; bi = r; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sb[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int nw = blockDim.x >> 5;
+    best = threadIdx.x < nw ? sb[threadIdx.x] : -2.0;
+    bi = threadIdx.x < nw ? si[threadIdx.x] : np_;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (threadIdx.x == 0) {
+      prs = bi;
+      up[bi] = 1;
+      perm[p * np_ + k] = bi;
+    }
+  }
+  __syncthreads();
+  const int pr = prs;
+  const double piv = Mp[(int64_t)pr * np_ + k];
+  if (piv == 0.0) {
+    if (threadIdx.x == 0) atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
+                                    (unsigned long long)(p + 1));
+    return;
+  }
+  const double rp = 1.0 / piv;
+  for (int c = threadIdx.x; c < np_; c += blockDim.x) {
+    const double v = (c == k) ? rp : Mp[(int64_t)pr * np_ + c] * rp;
+    prow[p * np_ + c] = v;
+    Mp[(int64_t)pr * np_ + c] = v;
+  }
+}
+
+__global__ void big_eliminate_kernel(int np_, int k, double* M, const int* perm,
+                                     const double* colk, const double* prow) {
+  const int64_t p = blockIdx.y;
+  double* Mp = M + p * (int64_t)np_ * np_;
+  const int pr = perm[p * np_ + k];
+  const double rp = prow[p * np_ + k];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)np_ * np_;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / np_), c = (int)(e - (int64_t)r * np_);
+    if (r == pr) continue;
+    const double f = colk[p * np_ + r];
+    Mp[e] = (c == k) ? -f * rp : fma(-f, prow[p * np_ + c], Mp[e]);
+  }
+}
+
+__global__ void big_finalize_kernel(int np_, int ld, const double* M, const int* perm,
+                                    double* inv) {
+  const int64_t p = blockIdx.y;
+  const double* Mp = M + p * (int64_t)np_ * np_;
+  const int* pp = perm + p * np_;
+  extern __shared__ int step_of_row[];
+  for (int k = threadIdx.x; k < np_; k += blockDim.x) step_of_row[pp[k]] = k;
+  __syncthreads();
+  double* out = inv + p * (int64_t)np_ * ld;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)np_ * np_;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / np_), c = (int)(e - (int64_t)r * np_);
+    out[(int64_t)pp[c] * ld + step_of_row[r]] = Mp[e];
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -661,11 +795,35 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
 
 template <int NP, int LD, int NC>
 void apply_dispatch(const DevPatchGroup& g, const double* d, double* Y, cudaStream_t s) {
-  constexpr int TPP = ((LD / 2 + 31) / 32) * 32;
-  constexpr int PPC = 128 / TPP;
-  const int grid = grid_for(g.n_patches, PPC);
-  vanka_apply_kernel<NP, LD, NC><<<grid, 128, 0, s>>>(g.n_patches, g.nodes, g.inv, d,
-                                                       Y + g.y_offset);
+  const int grid = grid_for(g.n_patches, ApplyShape<LD>::PPC);
+  vanka_apply_kernel<NP, LD, NC><<<grid, ApplyShape<LD>::BLK, 0, s>>>(g.n_patches, g.nodes,
+                                                                       g.inv, d, Y + g.y_offset);
+}
+
+// batched global-memory Gauss-Jordan for large patches (see big_* kernels)
+void factorize_big(const DevMatrix& A, const DevPatchGroup& g, int64_t* status, cudaStream_t s) {
+  const int np_ = g.np;
+  const int64_t n = g.n_patches;
+  double *M = nullptr, *colk = nullptr, *prow = nullptr;
+  int *used = nullptr, *perm = nullptr;
+  cudaMalloc(&M, sizeof(double) * n * np_ * np_);
+  cudaMalloc(&colk, sizeof(double) * n * np_);
+  cudaMalloc(&prow, sizeof(double) * n * np_);
+  cudaMalloc(&used, sizeof(int) * n * np_);
+  cudaMalloc(&perm, sizeof(int) * n * np_);
+  const dim3 grid(64, (unsigned)n);
+  big_gather_kernel<<<grid, 256, 0, s>>>(A, np_, g.npn, g.nodes, M, used);
+  for (int k = 0; k < np_; ++k) {
+    big_pivot_kernel<<<(unsigned)n, 512, 0, s>>>(np_, k, M, used, perm, colk, prow, status);
+    big_eliminate_kernel<<<grid, 256, 0, s>>>(np_, k, M, perm, colk, prow);
+  }
+  big_finalize_kernel<<<grid, 256, sizeof(int) * np_, s>>>(np_, g.ld, M, perm, g.inv);
+  cudaStreamSynchronize(s);
+  cudaFree(M);
+  cudaFree(colk);
+  cudaFree(prow);
+  cudaFree(used);
+  cudaFree(perm);
 }
 
 template <int NP, int NC, int TY, int TX>
@@ -686,8 +844,8 @@ void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y
 }
 
 bool vanka_supported(int nc, int np) {
-  return (nc == 3 && (np == 27 || np == 75 || np == 81)) || (nc == 4 && np == 108) ||
-         (nc == 2 && np == 18);
+  return (nc == 3 && (np == 27 || np == 75 || np == 81)) ||
+         (nc == 4 && (np == 108 || np == 500)) || (nc == 2 && np == 18);
 }
 
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
@@ -698,6 +856,7 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
   else if (A.nc == 4 && g.np == 108) factorize_dispatch<108, 4, 27, 12>(A, g, status, s);
   else if (A.nc == 2 && g.np == 18) factorize_dispatch<18, 2, 6, 6>(A, g, status, s);
   else if (A.nc == 3 && g.np == 81) factorize_dispatch<81, 3, 9, 27>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 500) factorize_big(A, g, status, s);
 }
 
 void launch_vanka_apply(const DevPatchGroup& g, int nc, const double* d, double* Y,
@@ -708,6 +867,7 @@ void launch_vanka_apply(const DevPatchGroup& g, int nc, const double* d, double*
   else if (nc == 4 && g.np == 108) apply_dispatch<108, 108, 4>(g, d, Y, s);
   else if (nc == 2 && g.np == 18) apply_dispatch<18, 18, 2>(g, d, Y, s);
   else if (nc == 3 && g.np == 81) apply_dispatch<81, 82, 3>(g, d, Y, s);
+  else if (nc == 4 && g.np == 500) apply_dispatch<500, 500, 4>(g, d, Y, s);
 }
 
 void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int64_t* goff,

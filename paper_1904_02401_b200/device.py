@@ -287,9 +287,11 @@ class DeviceMgSolver:
         if lvl.outflow is not None:
             with fem.single_blas():
                 local = model._outflow_blocks(lvl.outflow, U, mats, k, theta, d)
-            sl = fem.pattern_slots(lvl.pattern.indptr, lvl.pattern.indices,
-                                   lvl.outflow.conn).reshape(-1)
-            slots, inv = np.unique(sl, return_inverse=True)
+            if getattr(lvl, "_outflow_slots", None) is None:    # state independent
+                sl = fem.pattern_slots(lvl.pattern.indptr, lvl.pattern.indices,
+                                       lvl.outflow.conn).reshape(-1)
+                lvl._outflow_slots = np.unique(sl, return_inverse=True)
+            slots, inv = lvl._outflow_slots
             vals = np.zeros((len(slots), nc, nc))
             np.add.at(vals, inv, local.reshape(-1, nc, nc))
         params = np.array([mats.rho_f, mats.mu_f, mats.rho_s, mats.mu_s, mats.lam_s, k, theta])

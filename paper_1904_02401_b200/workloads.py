@@ -131,6 +131,10 @@ CONFIGS = {
     # 16x4x4 fine, solid block against the y=0/z=0 walls: smallest 3D case with solid
     "3d_tiny": Workload("3d_tiny", 3, (4.0, 1.0, 1.0), (4, 1, 1), 3, (1.0, 0.0, 0.0),
                         (2.0, 0.5, 0.5)),
+    # the reference's 3D default blocking: one-element fluid patches (108x108)
+    # and 2x2x2-cell solid patches (500x500)
+    "3d_tiny_multi": Workload("3d_tiny_multi", 3, (4.0, 1.0, 1.0), (4, 1, 1), 3, (1.0, 0.0, 0.0),
+                              (2.0, 0.5, 0.5), fluid_patches="one", solid_patches="multi"),
 }
 
 
