@@ -132,9 +132,11 @@ CONFIGS = {
     "3d_tiny": Workload("3d_tiny", 3, (4.0, 1.0, 1.0), (4, 1, 1), 3, (1.0, 0.0, 0.0),
                         (2.0, 0.5, 0.5)),
     # the reference's 3D default blocking: one-element fluid patches (108x108)
-    # and 2x2x2-cell solid patches (500x500)
-    "3d_tiny_multi": Workload("3d_tiny_multi", 3, (4.0, 1.0, 1.0), (4, 1, 1), 3, (1.0, 0.0, 0.0),
-                              (2.0, 0.5, 0.5), fluid_patches="one", solid_patches="multi"),
+    # and 2x2x2-cell solid patches (500x500), on a solid slab that is nested
+    # on every level (the 3d_tiny block is not: its level-1 solid macros
+    # contain fluid cells and their 500x500 blocks are near-singular)
+    "3d_slab_multi": Workload("3d_slab_multi", 3, (4.0, 1.0, 1.0), (4, 1, 1), 3, (1.0, 0.0, 0.0),
+                              (2.0, 1.0, 1.0), fluid_patches="one", solid_patches="multi"),
 }
 
 

@@ -17,7 +17,7 @@ from paper_1904_02401_b200 import device, workloads as W
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="no CUDA device")]
 
-SMALL = ["2d_mini", "2d_one", "3d_tiny", "3d_tiny_multi"]
+SMALL = ["2d_mini", "2d_one", "3d_tiny", "3d_slab_multi"]
 _SOLVERS = {}
 
 

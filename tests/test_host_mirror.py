@@ -11,7 +11,7 @@ from golden_util import sha, operator_checksums
 
 from paper_1904_02401_b200 import fem, mesh as mm, workloads as W
 
-SMALL = ["2d_mini", "2d_one", "3d_tiny", "3d_tiny_multi"]
+SMALL = ["2d_mini", "2d_one", "3d_tiny", "3d_slab_multi"]
 
 
 @pytest.mark.parametrize("name", SMALL)

@@ -12,7 +12,7 @@ from golden_util import vector_checksums
 from oracle import linsolve_oracle as orc
 from paper_1904_02401_b200 import workloads as W
 
-SMALL = ["2d_mini", "2d_one", "3d_tiny", "3d_tiny_multi"]
+SMALL = ["2d_mini", "2d_one", "3d_tiny", "3d_slab_multi"]
 
 
 @pytest.mark.parametrize("name", SMALL)
