@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
   constexpr int NPN = NP / NC, RT = (NP + TY - 1) / TY, CT = (NP + TX - 1) / TX, NT = TY * TX;
   static_assert(NT >= 32, "need at least one full warp");
   __shared__ int64_t slotB[NPN * NPN], slotP[NPN * NPN];
-  __shared__ double colk[NP], prow[NP];
+  __shared__ double colk[2][NP], prow[NP];
   __shared__ int used[NP], prow_of_step[NP], step_of_row[NP];
   __shared__ int piv_row;
   const int tid = threadIdx.x, ty = tid / TX, tx = tid - (tid / TX) * TX;
@@ -299,10 +299,12 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
       }
       M[i][j] = v;
     }
-  for (int k = 0; k < NP; ++k) {
-    // 1. owners of column k publish it
+  // column k is published into colk[k & 1] by its owners at the end of step
+  // k-1's elimination (look-ahead), so a pivot step needs three barriers
+  auto publish_column = [&](int k) {
     if (tx == k % TX) {
       const int jk = k / TX;
+      double* dst = colk[k & 1];
 #pragma unroll
       for (int i = 0; i < RT; ++i) {
         const int r = ty + TY * i;
@@ -310,16 +312,20 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
 #pragma unroll
         for (int j = 0; j < CT; ++j)
           if (j == jk) v = M[i][j];
-        if (r < NP) colk[r] = v;
+        if (r < NP) dst[r] = v;
       }
     }
+  };
+  publish_column(0);
+  for (int k = 0; k < NP; ++k) {
+    const double* ck = colk[k & 1];
     __syncthreads();
     // 2. pivot: largest |.| among unused rows, lowest index on ties
     if (tid < 32) {
       double best = -1.0;
       int bi = NP;
       for (int r = tid; r < NP; r += 32) {
-        const double v = used[r] ? -1.0 : fabs(colk[r]);
+        const double v = used[r] ? -1.0 : fabs(ck[r]);
         if (v > best) { best = v; bi = r; }
       }
 #pragma unroll
@@ -337,7 +343,7 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
     }
     __syncthreads();
     const int pr = piv_row;
-    const double piv = colk[pr];
+    const double piv = ck[pr];
     if (piv == 0.0) {
       if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
                               (unsigned long long)(p + 1));
@@ -365,7 +371,7 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
     for (int i = 0; i < RT; ++i) {
       const int r = ty + TY * i;
       if (r == pr || r >= NP) continue;
-      const double f = colk[r];
+      const double f = ck[r];
 #pragma unroll
       for (int j = 0; j < CT; ++j) {
         const int c = tx + TX * j;
@@ -373,8 +379,9 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
         M[i][j] = (c == k) ? -f * rp : fma(-f, prow[c], M[i][j]);
       }
     }
-    __syncthreads();
+    if (k + 1 < NP) publish_column(k + 1);
   }
+  __syncthreads();
   double* out = inv + p * (int64_t)NP * ld;
 #pragma unroll
   for (int i = 0; i < RT; ++i)

@@ -92,6 +92,11 @@ struct DevBuf {
     if (count == 0) return cudaSuccess;
     return cudaMalloc(&p, count * sizeof(T));
   }
+  // keep the allocation when the size is unchanged (re-factorisation)
+  cudaError_t ensure(size_t count) {
+    if (p != nullptr && n == count) return cudaSuccess;
+    return alloc(count);
+  }
   cudaError_t upload(const T* host, size_t count, cudaStream_t s) {
     cudaError_t e = alloc(count);
     if (e != cudaSuccess || count == 0) return e;
@@ -363,7 +368,7 @@ struct MgHandle {
       CK(cudaMemsetAsync(status.p, 0, sizeof(int64_t), stream));
       int64_t off = 0;
       for (auto& g : L.groups) {
-        CK(g->inv.alloc((size_t)g->n_patches * g->np * g->ld));
+        CK(g->inv.ensure((size_t)g->n_patches * g->np * g->ld));
         DevPatchGroup dg;
         dg.npn = g->npn;
         dg.np = g->np;
@@ -390,11 +395,11 @@ struct MgHandle {
     if (!C.host_dense.empty()) {
       CK(coarse_inv.upload(C.host_dense.data(), (size_t)n0 * n0, stream));
     } else {   // device-assembled coarse operator
-      CK(coarse_inv.alloc((size_t)n0 * n0));
+      CK(coarse_inv.ensure((size_t)n0 * n0));
       CK(cudaMemsetAsync(coarse_inv.p, 0, sizeof(double) * n0 * n0, stream));
       launch_split_to_dense(C.mat(), coarse_inv.p, stream);
     }
-    CK(coarse_work.alloc(2 * n0 + 2));
+    CK(coarse_work.ensure(2 * n0 + 2));
     dense_inverse(coarse_inv.p, n0, coarse_work.p, status.p, stream);
     CK(cudaGetLastError());
     int64_t st = 0;
@@ -403,9 +408,9 @@ struct MgHandle {
     if (st != 0) return fail(ALEFSI_ERR_SINGULAR, "singular coarse-level matrix");
     for (int l = 0; l < n_levels; ++l) {
       Level& L = lv[l];
-      CK(L.x.alloc(L.ndof()));
-      CK(L.b.alloc(L.ndof()));
-      CK(L.d.alloc(L.ndof()));
+      CK(L.x.ensure(L.ndof()));
+      CK(L.b.ensure(L.ndof()));
+      CK(L.d.ensure(L.ndof()));
     }
     factorized = true;
     graph_valid = false;
