@@ -122,6 +122,59 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
   }
 }
 
+// Half-warp per block row for the short 2D rows (NC = 3, ~16 blocks + ~19
+// pressure-extension entries): lane = 3*blk + r over 15 of 16 lanes, two
+// independent rows per warp double the loads in flight per warp.
+template <int NC, int MODE>
+__global__ void __launch_bounds__(256) spmv_half_kernel(int64_t n, const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ indices,
+                                                        const double* __restrict__ data,
+                                                        const int64_t* __restrict__ pp_ptr,
+                                                        const int32_t* __restrict__ pp_idx,
+                                                        const double* __restrict__ pp_val,
+                                                        const double* __restrict__ x,
+                                                        const double* __restrict__ b,
+                                                        double* __restrict__ y) {
+  constexpr int HL = 16, BPI = HL / NC;
+  const int lane = threadIdx.x & 31, hl = lane & (HL - 1);
+  const unsigned hmask = (lane < HL) ? 0x0000ffffu : 0xffff0000u;
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  if (row >= n) return;     // both halves of a warp exit together only at the tail
+  const int r = hl % NC, sub = hl / NC;
+  const int64_t beg = indptr[row], end = indptr[row + 1];
+  double acc = 0.0;
+  if (sub < BPI) {
+    for (int64_t blk = beg + sub; blk < end; blk += BPI) {
+      const int64_t col = __ldcs(indices + blk);
+      const double* v = data + blk * (NC * NC) + r * NC;
+      const double* xv = x + col * NC;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc = fma(__ldcs(v + c), __ldg(xv + c), acc);
+    }
+  }
+  double accp = 0.0;
+  if (pp_ptr != nullptr)
+    for (int64_t e = pp_ptr[row] + hl; e < pp_ptr[row + 1]; e += HL)
+      accp = fma(__ldcs(pp_val + e), __ldg(x + (int64_t)__ldcs(pp_idx + e) * NC), accp);
+  double out[NC];
+#pragma unroll
+  for (int rr = 0; rr < NC; ++rr) {
+    double v = (r == rr && sub < BPI) ? acc : 0.0;
+    if (rr == 0) v += accp;
+#pragma unroll
+    for (int o = HL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(hmask, v, o, HL);
+    out[rr] = v;
+  }
+  if (hl < NC) {
+    double v = out[0];
+#pragma unroll
+    for (int rr = 1; rr < NC; ++rr)
+      if (hl == rr) v = out[rr];
+    const int64_t o = row * NC + hl;
+    y[o] = MODE == 1 ? b[o] - v : v;
+  }
+}
+
 // Odd block size (NC = 3, 2D): a row's blocks are one contiguous run of
 // 9*nb doubles, streamed with fully coalesced 8-byte loads (lane l takes
 // elements l, l+32, ...); each lane keeps one partial sum per block row.
@@ -783,6 +836,16 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
   // 2D 3x3 operator (per-element index arithmetic and 8-byte x gathers), so
   // it is kept only for reference behind a switch that is off
   constexpr bool kUseFlat = false;
+  if constexpr (NC == 3) {
+    const int hgrid = grid_for(A.n_nodes * 16, 256);
+    if (mode == 0)
+      spmv_half_kernel<NC, 0><<<hgrid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+                                                    A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
+    else
+      spmv_half_kernel<NC, 1><<<hgrid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+                                                    A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
+    return;
+  }
   if constexpr (NC % 2 == 1 && kUseFlat) {
     if (mode == 0)
       spmv_flat_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
