@@ -42,16 +42,6 @@ __device__ __forceinline__ double block_sum_256(double v, double* red) {
 
 inline int grid_for(int64_t n, int per_block) { return (int)((n + per_block - 1) / per_block); }
 
-// Streaming 16-byte load: evict-first, with a 256-byte L2 prefetch hint (the
-// operator blocks and patch inverses are read once per sweep in long runs).
-__device__ __forceinline__ double2 ld_stream(const double2* p) {
-  double2 v;
-  asm("ld.global.cs.L2::256B.v2.f64 {%0, %1}, [%2];"
-               : "=d"(v.x), "=d"(v.y)
-               : "l"(p));
-  return v;
-}
-
 // --------------------------------------------------------------------------
 // Block-sparse matrix-vector product.  One warp per block row (mesh node).
 // NC = 4: lane = 4*blk + r, each lane streams one 32-byte block row
@@ -88,7 +78,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
       if constexpr (NC % 2 == 0) {
 #pragma unroll
         for (int c = 0; c < NC / 2; ++c) {
-          const double2 vv = ld_stream(reinterpret_cast<const double2*>(v) + c);
+          const double2 vv = __ldcs(reinterpret_cast<const double2*>(v) + c);
           const double2 xx = __ldg(reinterpret_cast<const double2*>(xv) + c);
           acc = fma(vv.x, xx.x, acc);
           acc = fma(vv.y, xx.y, acc);
@@ -274,7 +264,7 @@ __global__ void __launch_bounds__(ApplyShape<LD>::BLK) vanka_apply_kernel(
   double2 acc = make_double2(0.0, 0.0);
 #pragma unroll 12
   for (int j = 0; j < NP; ++j) {
-    const double2 v = ld_stream(col + j * (LD / 2));
+    const double2 v = __ldcs(col + j * (LD / 2));
     const double dj = ds[sub][j];
     acc.x = fma(v.x, dj, acc.x);
     acc.y = fma(v.y, dj, acc.y);
