@@ -172,6 +172,8 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     setup["warm_device_assembly"] = t1 - t0
     setup["warm_vanka_setup"] = time.perf_counter() - t1
+    for lvl in prob.levels:          # host geometry tables are not needed any more
+        lvl.G = None                 # (keeps N replicas' host memory in check)
     b_dev = torch.from_numpy(case.b).to(dev)
     x_dev = torch.empty_like(b_dev)
 
