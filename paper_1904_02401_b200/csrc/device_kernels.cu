@@ -299,86 +299,104 @@ __global__ void vanka_gather_kernel(int64_t ndof, int nc, const int64_t* __restr
 // pivot LAPACK's getrf would choose), and at the end
 //     inv[q(r)][p_c] = R[r][c],   q = p^{-1},
 // which is written directly in the column-major (ld) layout.
-template <int NP, int NC, int TY, int TX>
+// NPAT patches share one CTA (and every barrier): the three barriers of a
+// pivot step are amortised over NPAT independent eliminations.
+template <int NP, int NC, int TY, int TX, int NPAT>
 __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
     DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, RT = (NP + TY - 1) / TY, CT = (NP + TX - 1) / TX, NT = TY * TX;
-  static_assert(NT >= 32, "need at least one full warp");
-  __shared__ int64_t slotB[NPN * NPN], slotP[NPN * NPN];
-  __shared__ double colk[2][NP], prow[NP];
-  __shared__ int used[NP], prow_of_step[NP], step_of_row[NP];
-  __shared__ int piv_row;
+  static_assert(NT >= 32 * NPAT, "need one full warp per patch for the pivot search");
+  __shared__ int32_t slotB[NPAT][NPN * NPN], slotP[NPAT][NPN * NPN];
+  __shared__ double colk[NPAT][2][NP], prow[NPAT][NP];
+  __shared__ int used[NPAT][NP], prow_of_step[NPAT][NP], step_of_row[NPAT][NP];
+  __shared__ int piv_row[NPAT];
   const int tid = threadIdx.x, ty = tid / TX, tx = tid - (tid / TX) * TX;
-  const int64_t p = blockIdx.x;
-  if (p >= n_patches) return;
-  const int32_t* pn = nodes + p * NPN;
-  for (int t = tid; t < NPN * NPN; t += NT) {
-    const int a = t / NPN, b = t - a * NPN;
-    const int64_t ra = pn[a];
-    const int32_t cb = pn[b];
-    int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
-    }
-    slotB[t] = (lo < A.indptr[ra + 1] && A.indices[lo] == cb) ? lo : -1;
-    int64_t sp = -1;
-    if (slotB[t] < 0 && A.pp_indptr != nullptr) {
-      lo = A.pp_indptr[ra];
-      hi = A.pp_indptr[ra + 1];
+  int64_t pid[NPAT];
+  bool live[NPAT];
+#pragma unroll
+  for (int q = 0; q < NPAT; ++q) {
+    pid[q] = (int64_t)blockIdx.x * NPAT + q;
+    live[q] = pid[q] < n_patches;
+  }
+#pragma unroll
+  for (int q = 0; q < NPAT; ++q) {
+    if (!live[q]) continue;
+    const int32_t* pn = nodes + pid[q] * NPN;
+    for (int t = tid; t < NPN * NPN; t += NT) {
+      const int a = t / NPN, b = t - a * NPN;
+      const int64_t ra = pn[a];
+      const int32_t cb = pn[b];
+      int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
       while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
-        if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
+        if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
       }
-      if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) sp = lo;
+      slotB[q][t] = (lo < A.indptr[ra + 1] && A.indices[lo] == cb) ? (int32_t)lo : -1;
+      int64_t sp = -1;
+      if (slotB[q][t] < 0 && A.pp_indptr != nullptr) {
+        lo = A.pp_indptr[ra];
+        hi = A.pp_indptr[ra + 1];
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
+        }
+        if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) sp = lo;
+      }
+      slotP[q][t] = (int32_t)sp;
     }
-    slotP[t] = sp;
   }
-  for (int i = tid; i < NP; i += NT) used[i] = 0;
+  for (int i = tid; i < NPAT * NP; i += NT) used[i / NP][i % NP] = 0;
   __syncthreads();
-  double M[RT][CT];
+  double M[NPAT][RT][CT];
 #pragma unroll
-  for (int i = 0; i < RT; ++i)
+  for (int q = 0; q < NPAT; ++q)
 #pragma unroll
-    for (int j = 0; j < CT; ++j) {
-      const int r = ty + TY * i, c = tx + TX * j;
-      double v = 0.0;
-      if (r < NP && c < NP) {
-        const int a = r / NC, ci = r - a * NC, b = c / NC, cj = c - b * NC;
-        const int t = a * NPN + b;
-        if (slotB[t] >= 0) v = A.data[slotB[t] * (NC * NC) + ci * NC + cj];
-        else if (ci == 0 && cj == 0 && slotP[t] >= 0) v = A.pp_data[slotP[t]];
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        const int r = ty + TY * i, c = tx + TX * j;
+        double v = (r == c) ? 1.0 : 0.0;       // identity for a missing tail patch
+        if (live[q] && r < NP && c < NP) {
+          const int a = r / NC, ci = r - a * NC, b = c / NC, cj = c - b * NC;
+          const int t = a * NPN + b;
+          v = 0.0;
+          if (slotB[q][t] >= 0) v = A.data[(int64_t)slotB[q][t] * (NC * NC) + ci * NC + cj];
+          else if (ci == 0 && cj == 0 && slotP[q][t] >= 0) v = A.pp_data[slotP[q][t]];
+        }
+        M[q][i][j] = v;
       }
-      M[i][j] = v;
-    }
-  // column k is published into colk[k & 1] by its owners at the end of step
-  // k-1's elimination (look-ahead), so a pivot step needs three barriers
+  // column k is published into colk[q][k & 1] by its owners at the end of
+  // step k-1's elimination (look-ahead): three barriers per pivot step
   auto publish_column = [&](int k) {
     if (tx == k % TX) {
       const int jk = k / TX;
-      double* dst = colk[k & 1];
 #pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        const int r = ty + TY * i;
-        double v = 0.0;
+      for (int q = 0; q < NPAT; ++q) {
+        double* dst = colk[q][k & 1];
 #pragma unroll
-        for (int j = 0; j < CT; ++j)
-          if (j == jk) v = M[i][j];
-        if (r < NP) dst[r] = v;
+        for (int i = 0; i < RT; ++i) {
+          const int r = ty + TY * i;
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j < CT; ++j)
+            if (j == jk) v = M[q][i][j];
+          if (r < NP) dst[r] = v;
+        }
       }
     }
   };
   publish_column(0);
   for (int k = 0; k < NP; ++k) {
-    const double* ck = colk[k & 1];
     __syncthreads();
-    // 2. pivot: largest |.| among unused rows, lowest index on ties
-    if (tid < 32) {
+    // pivot of patch q by warp q: largest |.| among unused rows, lowest index on ties
+    const int wq = tid >> 5, lane = tid & 31;
+    if (wq < NPAT) {
+      const double* ck = colk[wq][k & 1];
       double best = -1.0;
       int bi = NP;
-      for (int r = tid; r < NP; r += 32) {
-        const double v = used[r] ? -1.0 : fabs(ck[r]);
+      for (int r = lane; r < NP; r += 32) {
+        const double v = used[wq][r] ? -1.0 : fabs(ck[r]);
         if (v > best) { best = v; bi = r; }
       }
 #pragma unroll
@@ -387,65 +405,79 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
-      if (tid == 0) {
-        piv_row = bi;
-        used[bi] = 1;
-        prow_of_step[k] = bi;
-        step_of_row[bi] = k;
+      if (lane == 0) {
+        piv_row[wq] = bi;
+        used[wq][bi] = 1;
+        prow_of_step[wq][k] = bi;
+        step_of_row[wq][bi] = k;
+        if (live[wq] && ck[bi] == 0.0)
+          atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
+                    (unsigned long long)(pid[wq] + 1));
       }
     }
     __syncthreads();
-    const int pr = piv_row;
-    const double piv = ck[pr];
-    if (piv == 0.0) {
-      if (tid == 0) atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
-                              (unsigned long long)(p + 1));
-      return;
+    int pr[NPAT];
+    double rp[NPAT];
+#pragma unroll
+    for (int q = 0; q < NPAT; ++q) {
+      pr[q] = piv_row[q];
+      const double piv = colk[q][k & 1][pr[q]];
+      rp[q] = piv != 0.0 ? 1.0 / piv : 0.0;   // singular: reported above, result unused
     }
-    const double rp = 1.0 / piv;
-    // 3. owners of the pivot row scale it and publish it
-    if (ty == pr % TY) {
-      const int ip = pr / TY;
+    // owners of each pivot row scale it and publish it
+#pragma unroll
+    for (int q = 0; q < NPAT; ++q) {
+      if (ty != pr[q] % TY) continue;
+      const int ip = pr[q] / TY;
 #pragma unroll
       for (int i = 0; i < RT; ++i) {
         if (i != ip) continue;
 #pragma unroll
         for (int j = 0; j < CT; ++j) {
           const int c = tx + TX * j;
-          const double v = (c == k) ? rp : M[i][j] * rp;
-          M[i][j] = v;
-          if (c < NP) prow[c] = v;
+          const double v = (c == k) ? rp[q] : M[q][i][j] * rp[q];
+          M[q][i][j] = v;
+          if (c < NP) prow[q][c] = v;
         }
       }
     }
     __syncthreads();
-    // 4. eliminate column k from every other row
+    // eliminate column k from every other row
 #pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      const int r = ty + TY * i;
-      if (r == pr || r >= NP) continue;
-      const double f = ck[r];
+    for (int q = 0; q < NPAT; ++q) {
+      const double* ck = colk[q][k & 1];
 #pragma unroll
-      for (int j = 0; j < CT; ++j) {
-        const int c = tx + TX * j;
-        if (c >= NP) continue;
-        M[i][j] = (c == k) ? -f * rp : fma(-f, prow[c], M[i][j]);
+      for (int i = 0; i < RT; ++i) {
+        const int r = ty + TY * i;
+        if (r == pr[q] || r >= NP) continue;
+        const double f = ck[r];
+#pragma unroll
+        for (int j = 0; j < CT; ++j) {
+          const int c = tx + TX * j;
+          if (c >= NP) continue;
+          M[q][i][j] = (c == k) ? -f * rp[q] : fma(-f, prow[q][c], M[q][i][j]);
+        }
       }
     }
     if (k + 1 < NP) publish_column(k + 1);
   }
   __syncthreads();
-  double* out = inv + p * (int64_t)NP * ld;
 #pragma unroll
-  for (int i = 0; i < RT; ++i)
+  for (int q = 0; q < NPAT; ++q) {
+    if (!live[q]) continue;
+    double* out = inv + pid[q] * (int64_t)NP * ld;
 #pragma unroll
-    for (int j = 0; j < CT; ++j) {
-      const int r = ty + TY * i, c = tx + TX * j;
-      if (r < NP && c < NP) out[(int64_t)prow_of_step[c] * ld + step_of_row[r]] = M[i][j];
-    }
-  if (ld > NP)
-    for (int col = tid; col < NP; col += NT)
-      for (int r = NP; r < ld; ++r) out[(int64_t)col * ld + r] = 0.0;
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        const int r = ty + TY * i, c = tx + TX * j;
+        if (r < NP && c < NP)
+          out[(int64_t)prow_of_step[q][c] * ld + step_of_row[q][r]] = M[q][i][j];
+      }
+    if (ld > NP)
+      for (int col = tid; col < NP; col += NT)
+        for (int r = NP; r < ld; ++r) out[(int64_t)col * ld + r] = 0.0;
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -896,10 +928,11 @@ void factorize_big(const DevMatrix& A, const DevPatchGroup& g, int64_t* status, 
   cudaFree(perm);
 }
 
-template <int NP, int NC, int TY, int TX>
+template <int NP, int NC, int TY, int TX, int NPAT>
 void factorize_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                         cudaStream_t s) {
-  vanka_factorize_rt_kernel<NP, NC, TY, TX><<<(unsigned)g.n_patches, TY * TX, 0, s>>>(
+  const unsigned grid = (unsigned)((g.n_patches + NPAT - 1) / NPAT);
+  vanka_factorize_rt_kernel<NP, NC, TY, TX, NPAT><<<grid, TY * TX, 0, s>>>(
       A, g.n_patches, g.nodes, g.inv, g.ld, status);
 }
 
@@ -921,11 +954,11 @@ bool vanka_supported(int nc, int np) {
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                             cudaStream_t s) {
   if (g.n_patches == 0) return;
-  if (A.nc == 3 && g.np == 27) factorize_dispatch<27, 3, 9, 9>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 75) factorize_dispatch<75, 3, 15, 15>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108) factorize_dispatch<108, 4, 27, 12>(A, g, status, s);
-  else if (A.nc == 2 && g.np == 18) factorize_dispatch<18, 2, 6, 6>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 81) factorize_dispatch<81, 3, 9, 27>(A, g, status, s);
+  if (A.nc == 3 && g.np == 27) factorize_dispatch<27, 3, 9, 9, 2>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 75) factorize_dispatch<75, 3, 15, 15, 2>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108) factorize_dispatch<108, 4, 27, 12, 2>(A, g, status, s);
+  else if (A.nc == 2 && g.np == 18) factorize_dispatch<18, 2, 6, 6, 1>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 81) factorize_dispatch<81, 3, 9, 27, 2>(A, g, status, s);
   else if (A.nc == 4 && g.np == 500) factorize_big(A, g, status, s);
 }
 
