@@ -111,6 +111,35 @@ def test_device_kernels_vs_oracle(name):
         np.testing.assert_allclose(xf.cpu().numpy(), x + add, rtol=1e-13, atol=1e-13)
 
 
+@pytest.mark.parametrize("nu_pre,nu_post,omega", [(0, 1, 0.5), (1, 0, 1.0), (3, 2, 0.7)])
+def test_device_vcycle_variants_vs_oracle(nu_pre, nu_post, omega):
+    """Smoothing counts and damping are parameters of the reference MgSolver /
+    VankaSmoother (linsolve.py:147, 232); every combination matches."""
+    case = get_case("3d_tiny")
+    s = device.DeviceMgSolver(case.mg_levels(), nu_pre=nu_pre, nu_post=nu_post, omega=omega)
+    mg = orc.MgOracle(case, nu_pre, nu_post, omega)
+    z, zo = s.dot(case.b), mg.dot(case.b)
+    assert np.linalg.norm(z - zo) <= 1e-12 * np.linalg.norm(zo)
+    x, st = s.gmres(case.b, rel_tol=1e-8, max_iter=250)
+    xo, so = orc.gmres(mg.A[-1], case.b, mg, rel_tol=1e-8, max_iter=250)
+    assert_history(st, so.residuals, so.iterations)
+    s.close()
+
+
+def test_single_level_hierarchy_is_a_direct_solve():
+    """A one-level hierarchy is the coarse solve alone: GMRES converges in one
+    iteration (SPEC: 'one-level hierarchy -> exact coarse solve')."""
+    case = get_case("2d_mini")
+    lv = case.mg_levels()[:1]
+    s = device.DeviceMgSolver(lv)
+    A = case.matrices[0].to_csr()
+    b = np.random.default_rng(3).standard_normal(A.shape[0])
+    x, st = s.gmres(b, rel_tol=1e-10, max_iter=5)
+    assert st.iterations == 1
+    assert np.linalg.norm(b - A @ x) <= 1e-9 * np.linalg.norm(b)
+    s.close()
+
+
 def test_reference_named_linear_stack_api():
     """newton.LinearStack / linsolve.gmres mirror the reference entry points
     (build_momentum + solve_momentum) and reproduce the golden history."""
