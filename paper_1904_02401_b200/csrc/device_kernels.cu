@@ -122,6 +122,55 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
   }
 }
 
+// Even block size with 32-bit block/entry offsets (nnzb * NC^2 < 2^31): same
+// lane mapping as spmv_kernel, fewer integer instructions per byte streamed —
+// the kernel is partly issue-limited when the 1 kW power cap lowers SM clocks.
+template <int NC, int MODE>
+__global__ void __launch_bounds__(256) spmv32_kernel(int64_t n, const int64_t* __restrict__ indptr,
+                                                     const int32_t* __restrict__ indices,
+                                                     const double* __restrict__ data,
+                                                     const int64_t* __restrict__ pp_ptr,
+                                                     const int32_t* __restrict__ pp_idx,
+                                                     const double* __restrict__ pp_val,
+                                                     const double* __restrict__ x,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ y) {
+  static_assert(NC % 2 == 0 && kWarp % NC == 0, "even block size");
+  constexpr int BPI = kWarp / NC, H = NC / 2;
+  const int lane = threadIdx.x & 31;
+  const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (row >= n) return;
+  const int r = lane % NC, sub = lane / NC;
+  const int beg = (int)indptr[row], end = (int)indptr[row + 1];
+  const double2* d2 = reinterpret_cast<const double2*>(data) + r * H;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  double acc = 0.0;
+  for (int blk = beg + sub; blk < end; blk += BPI) {
+    const int col = __ldcs(indices + blk);
+#pragma unroll
+    for (int c = 0; c < H; ++c) {
+      const double2 vv = __ldcs(d2 + blk * (NC * H) + c);
+      const double2 xx = __ldg(x2 + col * H + c);
+      acc = fma(vv.x, xx.x, acc);
+      acc = fma(vv.y, xx.y, acc);
+    }
+  }
+  double accp = 0.0;
+  if (pp_ptr != nullptr) {
+    const int pb = (int)pp_ptr[row], pe = (int)pp_ptr[row + 1];
+    for (int e = pb + lane; e < pe; e += kWarp)
+      accp = fma(__ldcs(pp_val + e), __ldg(x + __ldcs(pp_idx + e) * NC), accp);
+    accp = warp_sum(accp);
+  }
+#pragma unroll
+  for (int o = NC; o < kWarp; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane < NC) {
+    const double v = acc + (lane == 0 ? accp : 0.0);
+    const int o = row * NC + lane;
+    y[o] = MODE == 1 ? b[o] - v : v;
+  }
+}
+
 // Half-warp per block row for the short 2D rows (NC = 3, ~16 blocks + ~19
 // pressure-extension entries): lane = 3*blk + r over 15 of 16 lanes, two
 // independent rows per warp double the loads in flight per warp.
@@ -886,6 +935,19 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
       spmv_flat_kernel<NC, 1><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
                                                    A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
     return;
+  }
+  if constexpr (NC % 2 == 0) {
+    const bool idx32 = A.nnzb * NC * NC < ((int64_t)1 << 31) && A.nnz_pp < ((int64_t)1 << 31) &&
+                       A.n_nodes * NC < ((int64_t)1 << 31);
+    if (idx32) {
+      if (mode == 0)
+        spmv32_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+                                                  A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
+      else
+        spmv32_kernel<NC, 1><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+                                                  A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
+      return;
+    }
   }
   if (mode == 0)
     spmv_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
