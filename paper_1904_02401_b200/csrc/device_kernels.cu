@@ -529,6 +529,176 @@ __global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
   }
 }
 
+// Column-warp variant: warp w owns the strided column set {w + W*j} of every
+// row ty + 32*i (lane ty).  The warp owning column k+1 publishes it and picks
+// the next pivot with a warp-local argmax right after its own share of the
+// step-k elimination, overlapped with the other warps' eliminations — two
+// block barriers per pivot step, no single-warp phase on the critical path.
+template <int NP, int NC, int W, int NPAT>
+__global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
+    DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
+    int ld, int64_t* status) {
+  constexpr int NPN = NP / NC, RT = (NP + 31) / 32, CT = (NP + W - 1) / W, NT = 32 * W;
+  __shared__ int32_t slotB[NPAT][NPN * NPN], slotP[NPAT][NPN * NPN];
+  __shared__ double colk[NPAT][2][NP], prow[NPAT][NP];
+  __shared__ int used[NPAT][NP], piv_of_step[NPAT][NP], step_of_row[NPAT][NP];
+  const int tid = threadIdx.x, ty = tid & 31, w = tid >> 5;
+  int64_t pid[NPAT];
+  bool live[NPAT];
+#pragma unroll
+  for (int q = 0; q < NPAT; ++q) {
+    pid[q] = (int64_t)blockIdx.x * NPAT + q;
+    live[q] = pid[q] < n_patches;
+  }
+#pragma unroll
+  for (int q = 0; q < NPAT; ++q) {
+    if (!live[q]) continue;
+    const int32_t* pn = nodes + pid[q] * NPN;
+    for (int t = tid; t < NPN * NPN; t += NT) {
+      const int a = t / NPN, b = t - a * NPN;
+      const int64_t ra = pn[a];
+      const int32_t cb = pn[b];
+      int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
+      }
+      slotB[q][t] = (lo < A.indptr[ra + 1] && A.indices[lo] == cb) ? (int32_t)lo : -1;
+      int64_t sp = -1;
+      if (slotB[q][t] < 0 && A.pp_indptr != nullptr) {
+        lo = A.pp_indptr[ra];
+        hi = A.pp_indptr[ra + 1];
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
+        }
+        if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) sp = lo;
+      }
+      slotP[q][t] = (int32_t)sp;
+    }
+  }
+  for (int i = tid; i < NPAT * NP; i += NT) used[i / NP][i % NP] = 0;
+  __syncthreads();
+  double M[NPAT][RT][CT];
+#pragma unroll
+  for (int q = 0; q < NPAT; ++q)
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        const int r = ty + 32 * i, c = w + W * j;
+        double v = (r == c) ? 1.0 : 0.0;          // identity for a missing tail patch
+        if (live[q] && r < NP && c < NP) {
+          const int a = r / NC, ci = r - a * NC, b = c / NC, cj = c - b * NC;
+          const int t = a * NPN + b;
+          v = 0.0;
+          if (slotB[q][t] >= 0) v = A.data[(int64_t)slotB[q][t] * (NC * NC) + ci * NC + cj];
+          else if (ci == 0 && cj == 0 && slotP[q][t] >= 0) v = A.pp_data[slotP[q][t]];
+        }
+        M[q][i][j] = v;
+      }
+  // owner warp of column k: publish it and choose its pivot (largest |.| of
+  // the unused rows, lowest index on ties)
+  auto owner_step = [&](int k) {
+    if (w != k % W) return;
+    const int jk = k / W;
+#pragma unroll
+    for (int q = 0; q < NPAT; ++q) {
+      double best = -1.0;
+      int bi = NP;
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = ty + 32 * i;
+        double v = 0.0;
+#pragma unroll
+        for (int j = 0; j < CT; ++j)
+          if (j == jk) v = M[q][i][j];
+        if (r < NP) {
+          colk[q][k & 1][r] = v;
+          const double a = used[q][r] ? -1.0 : fabs(v);
+          if (a > best) { best = a; bi = r; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (ty == 0) {
+        used[q][bi] = 1;
+        piv_of_step[q][k] = bi;
+        step_of_row[q][bi] = k;
+      }
+    }
+  };
+  owner_step(0);
+  for (int k = 0; k < NP; ++k) {
+    __syncthreads();
+    int pr[NPAT];
+    double rp[NPAT];
+#pragma unroll
+    for (int q = 0; q < NPAT; ++q) {
+      pr[q] = piv_of_step[q][k];
+      const double piv = colk[q][k & 1][pr[q]];
+      if (piv == 0.0 && live[q] && tid == 0)
+        atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
+                  (unsigned long long)(pid[q] + 1));
+      rp[q] = piv != 0.0 ? 1.0 / piv : 0.0;   // singular: reported, result unused
+      // one lane per warp holds the pivot row's elements of its columns
+      if (ty == (pr[q] & 31)) {
+        const int ip = pr[q] >> 5;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          if (i != ip) continue;
+#pragma unroll
+          for (int j = 0; j < CT; ++j) {
+            const int c = w + W * j;
+            const double v = (c == k) ? rp[q] : M[q][i][j] * rp[q];
+            M[q][i][j] = v;
+            if (c < NP) prow[q][c] = v;
+          }
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NPAT; ++q) {
+      const double* ck = colk[q][k & 1];
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = ty + 32 * i;
+        if (r == pr[q] || r >= NP) continue;
+        const double f = ck[r];
+#pragma unroll
+        for (int j = 0; j < CT; ++j) {
+          const int c = w + W * j;
+          if (c >= NP) continue;
+          M[q][i][j] = (c == k) ? -f * rp[q] : fma(-f, prow[q][c], M[q][i][j]);
+        }
+      }
+    }
+    if (k + 1 < NP) owner_step(k + 1);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NPAT; ++q) {
+    if (!live[q]) continue;
+    double* out = inv + pid[q] * (int64_t)NP * ld;
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        const int r = ty + 32 * i, c = w + W * j;
+        if (r < NP && c < NP)
+          out[(int64_t)piv_of_step[q][c] * ld + step_of_row[q][r]] = M[q][i][j];
+      }
+    if (ld > NP)
+      for (int col = tid; col < NP; col += NT)
+        for (int r = NP; r < ld; ++r) out[(int64_t)col * ld + r] = 0.0;
+  }
+}
+
 // --------------------------------------------------------------------------
 // Large patches (2x2x2-cell macros in 3D: 500 x 500): batched Gauss-Jordan
 // in global memory, one pivot step per launch pair over all patches of the
@@ -990,6 +1160,14 @@ void factorize_big(const DevMatrix& A, const DevPatchGroup& g, int64_t* status, 
   cudaFree(perm);
 }
 
+template <int NP, int NC, int W, int NPAT>
+void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
+                           cudaStream_t s) {
+  const unsigned grid = (unsigned)((g.n_patches + NPAT - 1) / NPAT);
+  vanka_factorize_cw_kernel<NP, NC, W, NPAT><<<grid, 32 * W, 0, s>>>(A, g.n_patches, g.nodes,
+                                                                    g.inv, g.ld, status);
+}
+
 template <int NP, int NC, int TY, int TX, int NPAT>
 void factorize_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                         cudaStream_t s) {
@@ -1016,11 +1194,11 @@ bool vanka_supported(int nc, int np) {
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                             cudaStream_t s) {
   if (g.n_patches == 0) return;
-  if (A.nc == 3 && g.np == 27) factorize_dispatch<27, 3, 9, 9, 2>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 75) factorize_dispatch<75, 3, 15, 15, 2>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108) factorize_dispatch<108, 4, 27, 12, 2>(A, g, status, s);
-  else if (A.nc == 2 && g.np == 18) factorize_dispatch<18, 2, 6, 6, 1>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 81) factorize_dispatch<81, 3, 9, 27, 2>(A, g, status, s);
+  if (A.nc == 3 && g.np == 27) factorize_cw_dispatch<27, 3, 3, 2>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 75) factorize_cw_dispatch<75, 3, 8, 2>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108) factorize_cw_dispatch<108, 4, 12, 1>(A, g, status, s);
+  else if (A.nc == 2 && g.np == 18) factorize_cw_dispatch<18, 2, 2, 2>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 81) factorize_cw_dispatch<81, 3, 9, 2>(A, g, status, s);
   else if (A.nc == 4 && g.np == 500) factorize_big(A, g, status, s);
 }
 
