@@ -539,10 +539,13 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
     DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, RT = (NP + 31) / 32, CT = (NP + W - 1) / W, NT = 32 * W;
+  constexpr int NR = 32 * RT, NCOL = W * CT;               // padded row / column counts
   __shared__ int32_t slotB[NPAT][NPN * NPN], slotP[NPAT][NPN * NPN];
-  __shared__ double colk[NPAT][2][NP], prow[NPAT][NP];
+  __shared__ double colk[NPAT][2][NR], prow[NPAT][NCOL];
   __shared__ int used[NPAT][NP], piv_of_step[NPAT][NP], step_of_row[NPAT][NP];
   const int tid = threadIdx.x, ty = tid & 31, w = tid >> 5;
+  for (int i = tid; i < NPAT * 2 * NR; i += NT) (&colk[0][0][0])[i] = 0.0;
+  for (int i = tid; i < NPAT * NCOL; i += NT) (&prow[0][0])[i] = 0.0;
   int64_t pid[NPAT];
   bool live[NPAT];
 #pragma unroll
@@ -662,19 +665,29 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
       }
     }
     __syncthreads();
+    // branch-free elimination: padded rows hold f = 0 (colk zero-padded) and
+    // padded columns multiply a zero prow entry; the pivot row keeps its
+    // scaled values through f = 0 and the select on column k
 #pragma unroll
     for (int q = 0; q < NPAT; ++q) {
       const double* ck = colk[q][k & 1];
+      double pv[CT];
+      bool isk[CT];
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        pv[j] = prow[q][w + W * j];
+        isk[j] = (w + W * j) == k;
+      }
 #pragma unroll
       for (int i = 0; i < RT; ++i) {
         const int r = ty + 32 * i;
-        if (r == pr[q] || r >= NP) continue;
-        const double f = ck[r];
+        const bool piv_row = r == pr[q];
+        const double f = piv_row ? 0.0 : ck[r];
+        const double fk = -f * rp[q];
 #pragma unroll
         for (int j = 0; j < CT; ++j) {
-          const int c = w + W * j;
-          if (c >= NP) continue;
-          M[q][i][j] = (c == k) ? -f * rp[q] : fma(-f, prow[q][c], M[q][i][j]);
+          const double upd = fma(-f, pv[j], M[q][i][j]);
+          M[q][i][j] = (isk[j] && !piv_row) ? fk : upd;
         }
       }
     }
