@@ -224,57 +224,6 @@ __global__ void __launch_bounds__(256) spmv_half_kernel(int64_t n, const int64_t
   }
 }
 
-// Odd block size (NC = 3, 2D): a row's blocks are one contiguous run of
-// 9*nb doubles, streamed with fully coalesced 8-byte loads (lane l takes
-// elements l, l+32, ...); each lane keeps one partial sum per block row.
-template <int NC, int MODE>
-__global__ void __launch_bounds__(256) spmv_flat_kernel(int64_t n, const int64_t* __restrict__ indptr,
-                                                        const int32_t* __restrict__ indices,
-                                                        const double* __restrict__ data,
-                                                        const int64_t* __restrict__ pp_ptr,
-                                                        const int32_t* __restrict__ pp_idx,
-                                                        const double* __restrict__ pp_val,
-                                                        const double* __restrict__ x,
-                                                        const double* __restrict__ b,
-                                                        double* __restrict__ y) {
-  constexpr int BS = NC * NC;
-  const int lane = threadIdx.x & 31;
-  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= n) return;
-  const int64_t beg = indptr[row], end = indptr[row + 1];
-  const int64_t ne = (end - beg) * BS;
-  const double* rd = data + beg * BS;
-  double acc[NC];
-#pragma unroll
-  for (int r = 0; r < NC; ++r) acc[r] = 0.0;
-#pragma unroll 4
-  for (int64_t e = lane; e < ne; e += kWarp) {
-    const int64_t blk = e / BS;
-    const int w = (int)(e - blk * BS);
-    const int r = w / NC, c = w - r * NC;
-    const double v = __ldcs(rd + e) * __ldg(x + (int64_t)__ldg(indices + beg + blk) * NC + c);
-#pragma unroll
-    for (int rr = 0; rr < NC; ++rr)
-      if (rr == r) acc[rr] += v;
-  }
-  double accp = 0.0;
-  if (pp_ptr != nullptr) {
-    for (int64_t e = pp_ptr[row] + lane; e < pp_ptr[row + 1]; e += kWarp)
-      accp = fma(__ldcs(pp_val + e), __ldg(x + (int64_t)__ldcs(pp_idx + e) * NC), accp);
-  }
-  acc[0] += accp;
-#pragma unroll
-  for (int rr = 0; rr < NC; ++rr) acc[rr] = warp_sum(acc[rr]);
-  if (lane < NC) {
-    double v = acc[0];
-#pragma unroll
-    for (int rr = 1; rr < NC; ++rr)
-      if (lane == rr) v = acc[rr];
-    const int64_t o = row * NC + lane;
-    y[o] = MODE == 1 ? b[o] - v : v;
-  }
-}
-
 // --------------------------------------------------------------------------
 // Vanka apply: Y[p] = A_p^{-1} d[dofs_p].  Inverses are stored column-major
 // with an even column length LD, so thread t of a patch owns rows 2t, 2t+1
@@ -340,199 +289,16 @@ __global__ void vanka_gather_kernel(int64_t ndof, int nc, const int64_t* __restr
   x[t] = __dadd_rn(base, __dmul_rn(omega, acc));
 }
 
-// Register-tiled Gauss-Jordan inversion with implicit partial pivoting.
-// A TY x TX thread grid owns the patch matrix in registers (thread (ty,tx)
-// holds rows ty+TY*i, columns tx+TX*j); per pivot step only the pivot column
-// and the scaled pivot row go through shared memory.  Rows are never
-// swapped: step k pivots on the largest unused row p_k of column k (the
-// pivot LAPACK's getrf would choose), and at the end
+// Gauss-Jordan inversion of every patch matrix with implicit partial
+// pivoting, one CTA of W warps per NPAT patches.  Rows are never swapped:
+// step k pivots on the largest unused row p_k of column k (the pivot LAPACK's
+// getrf would choose, lowest index on ties), and at the end
 //     inv[q(r)][p_c] = R[r][c],   q = p^{-1},
 // which is written directly in the column-major (ld) layout.
-// NPAT patches share one CTA (and every barrier): the three barriers of a
-// pivot step are amortised over NPAT independent eliminations.
-template <int NP, int NC, int TY, int TX, int NPAT>
-__global__ void __launch_bounds__(TY* TX) vanka_factorize_rt_kernel(
-    DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
-    int ld, int64_t* status) {
-  constexpr int NPN = NP / NC, RT = (NP + TY - 1) / TY, CT = (NP + TX - 1) / TX, NT = TY * TX;
-  static_assert(NT >= 32 * NPAT, "need one full warp per patch for the pivot search");
-  __shared__ int32_t slotB[NPAT][NPN * NPN], slotP[NPAT][NPN * NPN];
-  __shared__ double colk[NPAT][2][NP], prow[NPAT][NP];
-  __shared__ int used[NPAT][NP], prow_of_step[NPAT][NP], step_of_row[NPAT][NP];
-  __shared__ int piv_row[NPAT];
-  const int tid = threadIdx.x, ty = tid / TX, tx = tid - (tid / TX) * TX;
-  int64_t pid[NPAT];
-  bool live[NPAT];
-#pragma unroll
-  for (int q = 0; q < NPAT; ++q) {
-    pid[q] = (int64_t)blockIdx.x * NPAT + q;
-    live[q] = pid[q] < n_patches;
-  }
-#pragma unroll
-  for (int q = 0; q < NPAT; ++q) {
-    if (!live[q]) continue;
-    const int32_t* pn = nodes + pid[q] * NPN;
-    for (int t = tid; t < NPN * NPN; t += NT) {
-      const int a = t / NPN, b = t - a * NPN;
-      const int64_t ra = pn[a];
-      const int32_t cb = pn[b];
-      int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
-      }
-      slotB[q][t] = (lo < A.indptr[ra + 1] && A.indices[lo] == cb) ? (int32_t)lo : -1;
-      int64_t sp = -1;
-      if (slotB[q][t] < 0 && A.pp_indptr != nullptr) {
-        lo = A.pp_indptr[ra];
-        hi = A.pp_indptr[ra + 1];
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
-        }
-        if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) sp = lo;
-      }
-      slotP[q][t] = (int32_t)sp;
-    }
-  }
-  for (int i = tid; i < NPAT * NP; i += NT) used[i / NP][i % NP] = 0;
-  __syncthreads();
-  double M[NPAT][RT][CT];
-#pragma unroll
-  for (int q = 0; q < NPAT; ++q)
-#pragma unroll
-    for (int i = 0; i < RT; ++i)
-#pragma unroll
-      for (int j = 0; j < CT; ++j) {
-        const int r = ty + TY * i, c = tx + TX * j;
-        double v = (r == c) ? 1.0 : 0.0;       // identity for a missing tail patch
-        if (live[q] && r < NP && c < NP) {
-          const int a = r / NC, ci = r - a * NC, b = c / NC, cj = c - b * NC;
-          const int t = a * NPN + b;
-          v = 0.0;
-          if (slotB[q][t] >= 0) v = A.data[(int64_t)slotB[q][t] * (NC * NC) + ci * NC + cj];
-          else if (ci == 0 && cj == 0 && slotP[q][t] >= 0) v = A.pp_data[slotP[q][t]];
-        }
-        M[q][i][j] = v;
-      }
-  // column k is published into colk[q][k & 1] by its owners at the end of
-  // step k-1's elimination (look-ahead): three barriers per pivot step
-  auto publish_column = [&](int k) {
-    if (tx == k % TX) {
-      const int jk = k / TX;
-#pragma unroll
-      for (int q = 0; q < NPAT; ++q) {
-        double* dst = colk[q][k & 1];
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const int r = ty + TY * i;
-          double v = 0.0;
-#pragma unroll
-          for (int j = 0; j < CT; ++j)
-            if (j == jk) v = M[q][i][j];
-          if (r < NP) dst[r] = v;
-        }
-      }
-    }
-  };
-  publish_column(0);
-  for (int k = 0; k < NP; ++k) {
-    __syncthreads();
-    // pivot of patch q by warp q: largest |.| among unused rows, lowest index on ties
-    const int wq = tid >> 5, lane = tid & 31;
-    if (wq < NPAT) {
-      const double* ck = colk[wq][k & 1];
-      double best = -1.0;
-      int bi = NP;
-      for (int r = lane; r < NP; r += 32) {
-        const double v = used[wq][r] ? -1.0 : fabs(ck[r]);
-        if (v > best) { best = v; bi = r; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      if (lane == 0) {
-        piv_row[wq] = bi;
-        used[wq][bi] = 1;
-        prow_of_step[wq][k] = bi;
-        step_of_row[wq][bi] = k;
-        if (live[wq] && ck[bi] == 0.0)
-          atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
-                    (unsigned long long)(pid[wq] + 1));
-      }
-    }
-    __syncthreads();
-    int pr[NPAT];
-    double rp[NPAT];
-#pragma unroll
-    for (int q = 0; q < NPAT; ++q) {
-      pr[q] = piv_row[q];
-      const double piv = colk[q][k & 1][pr[q]];
-      rp[q] = piv != 0.0 ? 1.0 / piv : 0.0;   // singular: reported above, result unused
-    }
-    // owners of each pivot row scale it and publish it
-#pragma unroll
-    for (int q = 0; q < NPAT; ++q) {
-      if (ty != pr[q] % TY) continue;
-      const int ip = pr[q] / TY;
-#pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        if (i != ip) continue;
-#pragma unroll
-        for (int j = 0; j < CT; ++j) {
-          const int c = tx + TX * j;
-          const double v = (c == k) ? rp[q] : M[q][i][j] * rp[q];
-          M[q][i][j] = v;
-          if (c < NP) prow[q][c] = v;
-        }
-      }
-    }
-    __syncthreads();
-    // eliminate column k from every other row
-#pragma unroll
-    for (int q = 0; q < NPAT; ++q) {
-      const double* ck = colk[q][k & 1];
-#pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        const int r = ty + TY * i;
-        if (r == pr[q] || r >= NP) continue;
-        const double f = ck[r];
-#pragma unroll
-        for (int j = 0; j < CT; ++j) {
-          const int c = tx + TX * j;
-          if (c >= NP) continue;
-          M[q][i][j] = (c == k) ? -f * rp[q] : fma(-f, prow[q][c], M[q][i][j]);
-        }
-      }
-    }
-    if (k + 1 < NP) publish_column(k + 1);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NPAT; ++q) {
-    if (!live[q]) continue;
-    double* out = inv + pid[q] * (int64_t)NP * ld;
-#pragma unroll
-    for (int i = 0; i < RT; ++i)
-#pragma unroll
-      for (int j = 0; j < CT; ++j) {
-        const int r = ty + TY * i, c = tx + TX * j;
-        if (r < NP && c < NP)
-          out[(int64_t)prow_of_step[q][c] * ld + step_of_row[q][r]] = M[q][i][j];
-      }
-    if (ld > NP)
-      for (int col = tid; col < NP; col += NT)
-        for (int r = NP; r < ld; ++r) out[(int64_t)col * ld + r] = 0.0;
-  }
-}
-
-// Column-warp variant: warp w owns the strided column set {w + W*j} of every
-// row ty + 32*i (lane ty).  The warp owning column k+1 publishes it and picks
-// the next pivot with a warp-local argmax right after its own share of the
-// step-k elimination, overlapped with the other warps' eliminations — two
+// Warp w owns the strided column set {w + W*j} of every row ty + 32*i (lane
+// ty), in registers.  The warp owning column k+1 publishes it and picks the
+// next pivot with a warp-local argmax right after its own share of the
+// step-k elimination, overlapped with the other warps' eliminations: two
 // block barriers per pivot step, no single-warp phase on the critical path.
 template <int NP, int NC, int W, int NPAT>
 __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
@@ -1096,10 +862,6 @@ template <int NC>
 void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
                    cudaStream_t s) {
   const int grid = grid_for(A.n_nodes * 32, 256);
-  // the flat variant measured 1.6x slower than the block-row kernel for the
-  // 2D 3x3 operator (per-element index arithmetic and 8-byte x gathers), so
-  // it is kept only for reference behind a switch that is off
-  constexpr bool kUseFlat = false;
   if constexpr (NC == 3) {
     const int hgrid = grid_for(A.n_nodes * 16, 256);
     if (mode == 0)
@@ -1108,15 +870,6 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
     else
       spmv_half_kernel<NC, 1><<<hgrid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
                                                     A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
-    return;
-  }
-  if constexpr (NC % 2 == 1 && kUseFlat) {
-    if (mode == 0)
-      spmv_flat_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
-                                                   A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
-    else
-      spmv_flat_kernel<NC, 1><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
-                                                   A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
     return;
   }
   if constexpr (NC % 2 == 0) {
@@ -1179,14 +932,6 @@ void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* 
   const unsigned grid = (unsigned)((g.n_patches + NPAT - 1) / NPAT);
   vanka_factorize_cw_kernel<NP, NC, W, NPAT><<<grid, 32 * W, 0, s>>>(A, g.n_patches, g.nodes,
                                                                     g.inv, g.ld, status);
-}
-
-template <int NP, int NC, int TY, int TX, int NPAT>
-void factorize_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
-                        cudaStream_t s) {
-  const unsigned grid = (unsigned)((g.n_patches + NPAT - 1) / NPAT);
-  vanka_factorize_rt_kernel<NP, NC, TY, TX, NPAT><<<grid, TY * TX, 0, s>>>(
-      A, g.n_patches, g.nodes, g.inv, g.ld, status);
 }
 
 }  // namespace
