@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device_kernels.cuh"
 
@@ -171,6 +172,89 @@ __global__ void __launch_bounds__(256) spmv32_kernel(int64_t n, const int64_t* _
   }
 }
 
+// 256-bit global loads (sm_100): one LDG.256 per block row and per x block.
+struct d4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ d4 ld256_stream(const double* p) {   // evict-first
+  d4 v;
+  asm("ld.global.L1::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ d4 ld256_ro(const double* p) {       // read-only path
+  d4 v;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+// NC = 4 with 32-bit offsets: lane = 4*blk + r loads its whole 32-byte block
+// row and the 32-byte x block with one instruction each (half the load
+// instructions of spmv32_kernel; same FMA order, bitwise-equal results).
+template <int MODE, bool SHFL>
+__global__ void __launch_bounds__(256) spmv4_v4_kernel(int64_t n, const int64_t* __restrict__ indptr,
+                                                       const int32_t* __restrict__ indices,
+                                                       const double* __restrict__ data,
+                                                       const int64_t* __restrict__ pp_ptr,
+                                                       const int32_t* __restrict__ pp_idx,
+                                                       const double* __restrict__ pp_val,
+                                                       const double* __restrict__ x,
+                                                       const double* __restrict__ b,
+                                                       double* __restrict__ y) {
+  constexpr int NC = 4, BPI = kWarp / NC;
+  const int lane = threadIdx.x & 31;
+  const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (row >= n) return;
+  const int r = lane % NC, sub = lane / NC;
+  const int beg = (int)indptr[row], end = (int)indptr[row + 1];
+  const double* dr = data + r * NC;
+  double acc = 0.0;
+  if constexpr (!SHFL) {
+    for (int blk = beg + sub; blk < end; blk += BPI) {
+      const int col = __ldcs(indices + blk);
+      const d4 vv = ld256_stream(dr + blk * (NC * NC));
+      const d4 xx = ld256_ro(x + col * NC);
+      acc = fma(vv.x, xx.x, acc);
+      acc = fma(vv.y, xx.y, acc);
+      acc = fma(vv.z, xx.z, acc);
+      acc = fma(vv.w, xx.w, acc);
+    }
+  }
+  // SHFL: block columns are fetched 32 at a time with one coalesced load and
+  // handed out by shuffle, so the x gather of an iteration waits on L2 only
+  if constexpr (SHFL) for (int base = beg; base < end; base += kWarp) {
+    const int cidx = base + lane < end ? __ldcs(indices + base + lane) : 0;
+#pragma unroll 1
+    for (int j = 0; j < kWarp / BPI; ++j) {
+      const int col = __shfl_sync(0xffffffffu, cidx, j * BPI + sub);
+      const int blk = base + j * BPI + sub;
+      if (blk < end) {
+        const d4 vv = ld256_stream(dr + blk * (NC * NC));
+        const d4 xx = ld256_ro(x + col * NC);
+        acc = fma(vv.x, xx.x, acc);
+        acc = fma(vv.y, xx.y, acc);
+        acc = fma(vv.z, xx.z, acc);
+        acc = fma(vv.w, xx.w, acc);
+      }
+    }
+  }
+  double accp = 0.0;
+  if (pp_ptr != nullptr) {
+    const int pb = (int)pp_ptr[row], pe = (int)pp_ptr[row + 1];
+    for (int e = pb + lane; e < pe; e += kWarp)
+      accp = fma(__ldcs(pp_val + e), __ldg(x + __ldcs(pp_idx + e) * NC), accp);
+    accp = warp_sum(accp);
+  }
+#pragma unroll
+  for (int o = NC; o < kWarp; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane < NC) {
+    const double v = acc + (lane == 0 ? accp : 0.0);
+    const int o = row * NC + lane;
+    y[o] = MODE == 1 ? b[o] - v : v;
+  }
+}
+
 // Half-warp per block row for the short 2D rows (NC = 3, ~16 blocks + ~19
 // pressure-extension entries): lane = 3*blk + r over 15 of 16 lanes, two
 // independent rows per warp double the loads in flight per warp.
@@ -226,26 +310,28 @@ __global__ void __launch_bounds__(256) spmv_half_kernel(int64_t n, const int64_t
 
 // --------------------------------------------------------------------------
 // Vanka apply: Y[p] = A_p^{-1} d[dofs_p].  Inverses are stored column-major
-// with an even column length LD, so thread t of a patch owns rows 2t, 2t+1
-// and streams one 16-byte pair per column: a patch column is one contiguous
-// LD*8-byte run, read exactly once per sweep with evict-first loads.  The
-// patch defect is staged in shared memory and broadcast.
+// with an even column length LD, so thread t of a patch owns rows
+// RPT*t .. RPT*t+RPT-1 and streams one 16-byte (RPT = 2) or 32-byte (RPT = 4,
+// LD % 4 == 0, 32-byte aligned storage) piece per column: a patch column is
+// one contiguous LD*8-byte run, read exactly once per sweep with evict-first
+// loads.  The patch defect is staged in shared memory and broadcast.
 // --------------------------------------------------------------------------
-template <int LD>
+template <int LD, int RPT>
 struct ApplyShape {
-  static constexpr int TPP = ((LD / 2 + 31) / 32) * 32;   // threads per patch
-  static constexpr int BLK = TPP > 128 ? TPP : 128;       // CTA size
-  static constexpr int PPC = BLK / TPP;                   // patches per CTA
+  static constexpr int TPP = ((LD / RPT + 31) / 32) * 32;  // threads per patch
+  static constexpr int BLK = TPP > 128 ? TPP : 128;        // CTA size
+  static constexpr int PPC = BLK / TPP;                    // patches per CTA
 };
 
-template <int NP, int LD, int NC>
-__global__ void __launch_bounds__(ApplyShape<LD>::BLK) vanka_apply_kernel(
+template <int NP, int LD, int NC, int RPT>
+__global__ void __launch_bounds__(ApplyShape<LD, RPT>::BLK) vanka_apply_kernel(
     int64_t n_patches, const int32_t* __restrict__ nodes, const double* __restrict__ inv,
     const double* __restrict__ d, double* __restrict__ Y) {
   constexpr int NPN = NP / NC;
-  constexpr int TPP = ApplyShape<LD>::TPP;
-  constexpr int PPC = ApplyShape<LD>::PPC;
+  constexpr int TPP = ApplyShape<LD, RPT>::TPP;
+  constexpr int PPC = ApplyShape<LD, RPT>::PPC;
   static_assert(PPC >= 1, "patch too large for one CTA");
+  static_assert(LD % RPT == 0 && (RPT == 2 || RPT == 4), "row split");
   __shared__ double ds[PPC][LD];
   const int sub = threadIdx.x / TPP, t = threadIdx.x % TPP;
   const int64_t p = (int64_t)blockIdx.x * PPC + sub;
@@ -257,17 +343,34 @@ __global__ void __launch_bounds__(ApplyShape<LD>::BLK) vanka_apply_kernel(
     }
   }
   __syncthreads();
-  if (!valid || 2 * t >= LD) return;
-  const double2* col = reinterpret_cast<const double2*>(inv + p * (int64_t)(NP * LD)) + t;
-  double2 acc = make_double2(0.0, 0.0);
+  if (!valid || RPT * t >= LD) return;
+  const double* col = inv + p * (int64_t)(NP * LD) + RPT * t;
+  double* out = Y + p * (int64_t)LD + RPT * t;
+  if constexpr (RPT == 2) {
+    double2 acc = make_double2(0.0, 0.0);
 #pragma unroll 12
-  for (int j = 0; j < NP; ++j) {
-    const double2 v = __ldcs(col + j * (LD / 2));
-    const double dj = ds[sub][j];
-    acc.x = fma(v.x, dj, acc.x);
-    acc.y = fma(v.y, dj, acc.y);
+    for (int j = 0; j < NP; ++j) {
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(col + j * LD));
+      const double dj = ds[sub][j];
+      acc.x = fma(v.x, dj, acc.x);
+      acc.y = fma(v.y, dj, acc.y);
+    }
+    *reinterpret_cast<double2*>(out) = acc;
+  } else {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 12
+    for (int j = 0; j < NP; ++j) {
+      const d4 v = ld256_stream(col + j * LD);
+      const double dj = ds[sub][j];
+      a0 = fma(v.x, dj, a0);
+      a1 = fma(v.y, dj, a1);
+      a2 = fma(v.z, dj, a2);
+      a3 = fma(v.w, dj, a3);
+    }
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(out), "d"(a0), "d"(a1), "d"(a2),
+                 "d"(a3)
+                 : "memory");
   }
-  reinterpret_cast<double2*>(Y + p * (int64_t)LD)[t] = acc;
 }
 
 // Deterministic scatter-add of the weighted patch corrections: each dof sums
@@ -858,6 +961,16 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
+// ALEFSI_SPMV_V4 (A/B measurement only): 0 = 2x128-bit kernel, 1 = 256-bit
+// loads, unset/2 = 256-bit loads + shuffled block columns
+int spmv_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("ALEFSI_SPMV_V4");
+    return e == nullptr ? 2 : (e[0] == '0' ? 0 : e[0] == '1' ? 1 : 2);
+  }();
+  return v;
+}
+
 template <int NC>
 void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
                    cudaStream_t s) {
@@ -875,6 +988,14 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
   if constexpr (NC % 2 == 0) {
     const bool idx32 = A.nnzb * NC * NC < ((int64_t)1 << 31) && A.nnz_pp < ((int64_t)1 << 31) &&
                        A.n_nodes * NC < ((int64_t)1 << 31);
+    const int var = spmv_variant();
+    if (idx32 && NC == 4 && var > 0) {
+      auto k = var == 1 ? (mode == 0 ? spmv4_v4_kernel<0, false> : spmv4_v4_kernel<1, false>)
+                        : (mode == 0 ? spmv4_v4_kernel<0, true> : spmv4_v4_kernel<1, true>);
+      k<<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr, A.pp_indices,
+                             A.pp_data, x, b, y);
+      return;
+    }
     if (idx32) {
       if (mode == 0)
         spmv32_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
@@ -893,11 +1014,30 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
                                             A.pp_indices, A.pp_data, x, b, y);
 }
 
+// ALEFSI_APPLY_V4=0 keeps 16-byte column pieces (A/B measurement only)
+bool apply_v4_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_APPLY_V4");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 template <int NP, int LD, int NC>
 void apply_dispatch(const DevPatchGroup& g, const double* d, double* Y, cudaStream_t s) {
-  const int grid = grid_for(g.n_patches, ApplyShape<LD>::PPC);
-  vanka_apply_kernel<NP, LD, NC><<<grid, ApplyShape<LD>::BLK, 0, s>>>(g.n_patches, g.nodes,
-                                                                       g.inv, d, Y + g.y_offset);
+  double* y = Y + g.y_offset;
+  if constexpr (LD % 4 == 0) {
+    if (apply_v4_enabled() && reinterpret_cast<uintptr_t>(g.inv) % 32 == 0 &&
+        reinterpret_cast<uintptr_t>(y) % 32 == 0) {
+      const int grid = grid_for(g.n_patches, ApplyShape<LD, 4>::PPC);
+      vanka_apply_kernel<NP, LD, NC, 4>
+          <<<grid, ApplyShape<LD, 4>::BLK, 0, s>>>(g.n_patches, g.nodes, g.inv, d, y);
+      return;
+    }
+  }
+  const int grid = grid_for(g.n_patches, ApplyShape<LD, 2>::PPC);
+  vanka_apply_kernel<NP, LD, NC, 2>
+      <<<grid, ApplyShape<LD, 2>::BLK, 0, s>>>(g.n_patches, g.nodes, g.inv, d, y);
 }
 
 // batched global-memory Gauss-Jordan for large patches (see big_* kernels)
