@@ -176,10 +176,10 @@ __global__ void __launch_bounds__(256) spmv32_kernel(int64_t n, const int64_t* _
 struct d4 {
   double x, y, z, w;
 };
-__device__ __forceinline__ d4 ld256_stream(const double* p) {   // evict-first
+__device__ __forceinline__ d4 ld256_stream(const double* p) {   // streamed: evict-first in L2
   d4 v;
-  asm("ld.global.L1::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  asm("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
   return v;
 }
 __device__ __forceinline__ d4 ld256_ro(const double* p) {       // read-only path
