@@ -392,6 +392,11 @@ __global__ void vanka_gather_kernel(int64_t ndof, int nc, const int64_t* __restr
   x[t] = __dadd_rn(base, __dmul_rn(omega, acc));
 }
 
+template <int I>
+struct IntC {
+  static constexpr int value = I;
+};
+
 // Gauss-Jordan inversion of every patch matrix with implicit partial
 // pivoting, one CTA of W warps per NPAT patches.  Rows are never swapped:
 // step k pivots on the largest unused row p_k of column k (the pivot LAPACK's
@@ -408,9 +413,10 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
     DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, RT = (NP + 31) / 32, CT = (NP + W - 1) / W, NT = 32 * W;
+  static_assert(RT <= 4, "pivot-row scaling covers up to 4 register rows");
   constexpr int NR = 32 * RT, NCOL = W * CT;               // padded row / column counts
   __shared__ int32_t slotB[NPAT][NPN * NPN], slotP[NPAT][NPN * NPN];
-  __shared__ double colk[NPAT][2][NR], prow[NPAT][NCOL];
+  __shared__ double colk[NPAT][2][NR], prow[NPAT][NCOL], pivval[NPAT];
   __shared__ int used[NPAT][NP], piv_of_step[NPAT][NP], step_of_row[NPAT][NP];
   const int tid = threadIdx.x, ty = tid & 31, w = tid >> 5;
   for (int i = tid; i < NPAT * 2 * NR; i += NT) (&colk[0][0][0])[i] = 0.0;
@@ -483,8 +489,12 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
         const int r = ty + 32 * i;
         double v = 0.0;
 #pragma unroll
-        for (int j = 0; j < CT; ++j)
+        for (int j = 0; j < CT; ++j) {
           if (j == jk) v = M[q][i][j];
+          // column k restarts from 0: the elimination's fma then yields
+          // -f * (1/pivot) there, with no per-element select
+          M[q][i][j] = (j == jk) ? 0.0 : M[q][i][j];
+        }
         if (r < NP) {
           colk[q][k & 1][r] = v;
           const double a = used[q][r] ? -1.0 : fabs(v);
@@ -497,10 +507,15 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
+      __syncwarp();
       if (ty == 0) {
         used[q][bi] = 1;
         piv_of_step[q][k] = bi;
         step_of_row[q][bi] = k;
+        // the pivot leaves the published column: f = 0 on the pivot row
+        // makes the elimination below select-free
+        pivval[q] = colk[q][k & 1][bi];
+        colk[q][k & 1][bi] = 0.0;
       }
     }
   };
@@ -512,17 +527,16 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
 #pragma unroll
     for (int q = 0; q < NPAT; ++q) {
       pr[q] = piv_of_step[q][k];
-      const double piv = colk[q][k & 1][pr[q]];
+      const double piv = pivval[q];
       if (piv == 0.0 && live[q] && tid == 0)
         atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
                   (unsigned long long)(pid[q] + 1));
       rp[q] = piv != 0.0 ? 1.0 / piv : 0.0;   // singular: reported, result unused
-      // one lane per warp holds the pivot row's elements of its columns
+      // one lane per warp holds the pivot row's elements of its columns; a
+      // branch per register row keeps the scaling straight-line code
       if (ty == (pr[q] & 31)) {
-        const int ip = pr[q] >> 5;
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          if (i != ip) continue;
+        auto scale = [&](auto I) {
+          constexpr int i = decltype(I)::value;
 #pragma unroll
           for (int j = 0; j < CT; ++j) {
             const int c = w + W * j;
@@ -530,34 +544,32 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
             M[q][i][j] = v;
             if (c < NP) prow[q][c] = v;
           }
+        };
+        switch (pr[q] >> 5) {
+          case 0: scale(IntC<0>{}); break;
+          case 1: if constexpr (RT > 1) scale(IntC<1>{}); break;
+          case 2: if constexpr (RT > 2) scale(IntC<2>{}); break;
+          default: if constexpr (RT > 3) scale(IntC<3>{}); break;
         }
       }
     }
     __syncthreads();
-    // branch-free elimination: padded rows hold f = 0 (colk zero-padded) and
-    // padded columns multiply a zero prow entry; the pivot row keeps its
-    // scaled values through f = 0 and the select on column k
+    // branch-free elimination: padded rows hold f = 0 (colk zero-padded),
+    // padded columns multiply a zero prow entry, the pivot row keeps its
+    // scaled values through f = 0 (its colk entry is cleared by the owner),
+    // and column k (zeroed by its owner, pivot entry 1/pivot in prow)
+    // becomes -f/pivot
 #pragma unroll
     for (int q = 0; q < NPAT; ++q) {
       const double* ck = colk[q][k & 1];
       double pv[CT];
-      bool isk[CT];
 #pragma unroll
-      for (int j = 0; j < CT; ++j) {
-        pv[j] = prow[q][w + W * j];
-        isk[j] = (w + W * j) == k;
-      }
+      for (int j = 0; j < CT; ++j) pv[j] = prow[q][w + W * j];
 #pragma unroll
       for (int i = 0; i < RT; ++i) {
-        const int r = ty + 32 * i;
-        const bool piv_row = r == pr[q];
-        const double f = piv_row ? 0.0 : ck[r];
-        const double fk = -f * rp[q];
+        const double nf = -ck[ty + 32 * i];
 #pragma unroll
-        for (int j = 0; j < CT; ++j) {
-          const double upd = fma(-f, pv[j], M[q][i][j]);
-          M[q][i][j] = (isk[j] && !piv_row) ? fk : upd;
-        }
+        for (int j = 0; j < CT; ++j) M[q][i][j] = fma(nf, pv[j], M[q][i][j]);
       }
     }
     if (k + 1 < NP) owner_step(k + 1);
