@@ -748,18 +748,24 @@ __global__ void transfer_kernel(int64_t nrows, int nc, const int64_t* __restrict
 // Coarse level: dense Gauss-Jordan inverse (one pivot step per launch pair)
 // and a warp-per-row dense matvec.
 // --------------------------------------------------------------------------
+// Pivot step k: one pass over column k (all rows, staged in shared memory)
+// finds the pivot among rows >= k; rows k and p are swapped, column k is
+// published with the swap applied, and the pivot row is scaled.
+constexpr int kGjMaxN = 4096;
 __global__ void __launch_bounds__(1024) gj_pivot_kernel(double* M, int64_t n, int64_t k,
                                                         int64_t* perm, double* colk,
                                                         double* rp_out, int64_t* status) {
   __shared__ double sb[32];
   __shared__ int64_t si[32];
   __shared__ int64_t prow;
+  __shared__ double cs[kGjMaxN];
   const int tid = threadIdx.x;
   double best = -1.0;
   int64_t bi = k;
-  for (int64_t i = k + tid; i < n; i += blockDim.x) {
-    const double v = fabs(M[i * n + k]);
-    if (v > best) { best = v; bi = i; }
+  for (int64_t i = tid; i < n; i += blockDim.x) {
+    const double v = M[i * n + k];
+    cs[i] = v;
+    if (i >= k && fabs(v) > best) { best = fabs(v); bi = i; }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -782,36 +788,48 @@ __global__ void __launch_bounds__(1024) gj_pivot_kernel(double* M, int64_t n, in
   }
   __syncthreads();
   const int64_t pr = prow;
-  if (pr != k)
-    for (int64_t j = tid; j < n; j += blockDim.x) {
-      const double t = M[k * n + j];
-      M[k * n + j] = M[pr * n + j];
-      M[pr * n + j] = t;
-    }
-  __syncthreads();
-  const double piv = M[k * n + k];
+  const double piv = cs[pr];
   if (piv == 0.0) {
     if (tid == 0 && *status == 0) *status = k + 1;
     if (tid == 0) *rp_out = 0.0;
     return;
   }
   const double rp = 1.0 / piv;
-  for (int64_t i = tid; i < n; i += blockDim.x) colk[i] = M[i * n + k];
-  __syncthreads();
-  for (int64_t j = tid; j < n; j += blockDim.x) M[k * n + j] = (j == k) ? rp : M[k * n + j] * rp;
+  for (int64_t i = tid; i < n; i += blockDim.x)
+    colk[i] = cs[i == k ? pr : (i == pr ? k : i)];
+  // swap rows k and pr, scale the new pivot row
+  for (int64_t j = tid; j < n; j += blockDim.x) {
+    const double vk = M[k * n + j], vp = M[pr * n + j];
+    if (pr != k) M[pr * n + j] = vk;
+    M[k * n + j] = (j == k) ? rp : vp * rp;
+  }
   if (tid == 0) *rp_out = rp;
 }
 
+// Elimination of column k from every row but k: row i = blockIdx.y, two
+// columns per thread (n even) with 16-byte accesses.
 __global__ void gj_eliminate_kernel(double* M, int64_t n, int64_t k, const double* colk,
                                     const double* rp_in) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n * n) return;
-  const int64_t i = e / n, j = e - i * n;
+  const int64_t i = blockIdx.y;
   if (i == k) return;
   const double rp = *rp_in;
   if (rp == 0.0) return;
   const double f = colk[i];
-  M[e] = (j == k) ? -f * rp : M[e] - f * M[k * n + j];
+  const double* pk = M + k * n;
+  double* row = M + i * n;
+  if ((n & 1) == 0) {
+    const int64_t j2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (2 * j2 >= n) return;
+    const double2 p = reinterpret_cast<const double2*>(pk)[j2];
+    double2 v = reinterpret_cast<double2*>(row)[j2];
+    v.x = (2 * j2 == k) ? -f * rp : v.x - f * p.x;
+    v.y = (2 * j2 + 1 == k) ? -f * rp : v.y - f * p.y;
+    reinterpret_cast<double2*>(row)[j2] = v;
+  } else {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+      row[j] = (j == k) ? -f * rp : row[j] - f * pk[j];
+  }
 }
 
 __global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm) {
@@ -1152,10 +1170,11 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
   double* rp = work + n;
   int64_t* perm = reinterpret_cast<int64_t*>(work + n + 1);
   cudaMemsetAsync(status, 0, sizeof(int64_t), s);
-  const int grid = grid_for(n * n, 256);
+  if (n > kGjMaxN) return (int)cudaErrorInvalidValue;
+  const dim3 grid((unsigned)grid_for((n + 1) / 2, 128), (unsigned)n);
   for (int64_t k = 0; k < n; ++k) {
     gj_pivot_kernel<<<1, 1024, 0, s>>>(M, n, k, perm, colk, rp, status);
-    gj_eliminate_kernel<<<grid, 256, 0, s>>>(M, n, k, colk, rp);
+    gj_eliminate_kernel<<<grid, 128, 0, s>>>(M, n, k, colk, rp);
   }
   gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm);
   return 0;

@@ -97,8 +97,10 @@ struct DevBuf {
     if (p != nullptr && n == count) return cudaSuccess;
     return alloc(count);
   }
+  // stream-ordered copy into a buffer kept across calls of the same size
+  // (no cudaFree, which would synchronise the device, per call)
   cudaError_t upload(const T* host, size_t count, cudaStream_t s) {
-    cudaError_t e = alloc(count);
+    cudaError_t e = ensure(count);
     if (e != cudaSuccess || count == 0) return e;
     return cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s);
   }
@@ -135,7 +137,8 @@ struct Level {
   bool has_asm = false;
   int dim = 0;
   DevBuf<int32_t> asm_cell_nodes, asm_group_cells;
-  DevBuf<double> asm_coords, asm_U, asm_Up, res_out;
+  DevBuf<double> asm_coords, asm_U, asm_Up, res_out, asm_extra_vals;
+  DevBuf<int64_t> asm_extra_slots;
   std::vector<int64_t> asm_group_ptr;
   std::vector<int> asm_group_kind;
   int64_t n_lps = 0;
@@ -400,7 +403,9 @@ struct MgHandle {
       launch_split_to_dense(C.mat(), coarse_inv.p, stream);
     }
     CK(coarse_work.ensure(2 * n0 + 2));
-    dense_inverse(coarse_inv.p, n0, coarse_work.p, status.p, stream);
+    if (dense_inverse(coarse_inv.p, n0, coarse_work.p, status.p, stream) != 0)
+      return fail(ALEFSI_ERR_ARG, "coarse level too large for the dense inverse (" +
+                                      std::to_string(n0) + " > 4096 dofs)");
     CK(cudaGetLastError());
     int64_t st = 0;
     CK(cudaMemcpyAsync(&st, status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
@@ -803,12 +808,10 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
   }
   CKAPI(cudaGetLastError());
   if (n_extra > 0) {
-    alefsi::DevBuf<int64_t> sl;
-    alefsi::DevBuf<double> vv;
-    CKAPI(sl.upload(extra_slots, n_extra, s));
-    CKAPI(vv.upload(extra_vals, (size_t)n_extra * nc * nc, s));
-    alefsi::launch_add_blocks(L.data.p, nc * nc, n_extra, sl.p, vv.p, s);
-    CKAPI(cudaStreamSynchronize(s));
+    CKAPI(L.asm_extra_slots.upload(extra_slots, n_extra, s));
+    CKAPI(L.asm_extra_vals.upload(extra_vals, (size_t)n_extra * nc * nc, s));
+    alefsi::launch_add_blocks(L.data.p, nc * nc, n_extra, L.asm_extra_slots.p,
+                              L.asm_extra_vals.p, s);
   }
   alefsi::launch_lps(L.data.p, nc, L.pp_data.p, L.n_lps, L.lps_cell.p, L.lps_pp.p, L.lps_val.p,
                      a.k, s);
