@@ -106,7 +106,15 @@ int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t n
  * asm_tables: Q2 basis N (nq,nb), gradients dN (nq,nb,dim), weights (nq).
  * asm_momentum: params = {rho_f, mu_f, rho_s, mu_s, lam_s, k, theta}; U and
  * U_prev host (n_nodes, 1+2dim); extra = host-reduced outflow-facet blocks
- * (unique slots).  The matrix must be re-factorised afterwards. */
+ * (unique slots; pass n_extra = 0 once asm_outflow has been called for the
+ * level).  The matrix must be re-factorised afterwards.
+ * asm_outflow (once per level): the do-nothing outflow facets
+ * (model._outflow_blocks, reference model.py:363-375) for assembly on the
+ * device: owner-cell nodes conn (n_facets, 3^dim) and cell ids, facet
+ * quadrature N (n_facets, nq, 3^dim), G (n_facets, nq, 3^dim, dim), dS
+ * (n_facets, nq), normal (n_facets, nq, dim), and the slot reduction plan:
+ * n_unique matrix slots, and per slot u the flat (facet, b, a) block indices
+ * contrib[uptr[u]:uptr[u+1]] in ascending order. */
 int alefsi_mg_asm_setup(alefsi_mg h, int32_t level, int32_t dim, int64_t n_cells,
                         const int32_t* cell_nodes, const double* coords, int32_t n_groups,
                         const int64_t* group_ptr, const int32_t* group_kind,
@@ -118,6 +126,11 @@ int alefsi_mg_asm_tables(alefsi_mg h, int32_t dim, int32_t nq, const double* N, 
 int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, const double* U,
                            const double* U_prev, int64_t n_extra, const int64_t* extra_slots,
                            const double* extra_vals);
+int alefsi_mg_asm_outflow(alefsi_mg h, int32_t level, int64_t n_facets, int32_t nq,
+                          const int32_t* conn, const int64_t* cells, const double* N,
+                          const double* G, const double* dS, const double* normal,
+                          int64_t n_unique, const int64_t* slots, const int64_t* uptr,
+                          const int64_t* contrib);
 /* Cell parts of the theta-step residual (which = 0, model.theta_residual,
  * reference model.py:208-275, out (n_nodes, 1+2dim)) or of the explicit
  * previous-state forces (which = 1, model.explicit_forces, model.py:159-185,

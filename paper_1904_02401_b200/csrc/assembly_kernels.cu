@@ -592,6 +592,94 @@ __global__ void __launch_bounds__(128) residual_cells_kernel(ResArgs a, const in
   }
 }
 
+// Do-nothing outflow correction of the Jacobian (reference model.py:363-375):
+// per outflow facet f and owner-cell basis pair (b, a)
+//   out[f,b,a,i,j] = sum_q coef_q N_qb (F^-T G_a)_qi (F^-T n)_qj,
+//   coef_q = -k theta mu_f J_q dS_q,  F = I + grad u at the facet points.
+// One CTA per facet; the (b, a, i, j) blocks go to a scratch array and are
+// reduced per matrix slot in a fixed order by outflow_reduce_kernel.
+template <int D>
+__global__ void __launch_bounds__(256) outflow_local_kernel(OutflowArgs a, double* out) {
+  constexpr int NB = D == 2 ? 9 : 27, NF = 1 + 2 * D, MQ = D == 2 ? 3 : 9;
+  __shared__ double u[NB][D], Gs[MQ][NB][D], Ns[MQ][NB], T[MQ][NB][D];
+  __shared__ double gu[MQ][D][D], Fi[MQ][D][D], Fin[MQ][D], coef[MQ];
+  const int64_t f = blockIdx.x;
+  const int nq = a.nq, tid = threadIdx.x;
+  for (int t = tid; t < NB * D; t += blockDim.x) {
+    const int b = t / D, i = t - b * D;
+    u[b][i] = a.U[(int64_t)a.conn[f * NB + b] * NF + 1 + D + i];
+  }
+  for (int t = tid; t < nq * NB; t += blockDim.x) {
+    const int q = t / NB, b = t - q * NB;
+    Ns[q][b] = a.N[f * nq * NB + t];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Gs[q][b][j] = a.G[(f * nq * NB + t) * D + j];
+  }
+  __syncthreads();
+  for (int t = tid; t < nq * D * D; t += blockDim.x) {
+    const int q = t / (D * D), i = (t / D) % D, j = t % D;
+    double acc = 0.0;
+    for (int b = 0; b < NB; ++b) acc = fma(Gs[q][b][j], u[b][i], acc);
+    gu[q][i][j] = acc;
+  }
+  __syncthreads();
+  if (tid < nq) {
+    const int q = tid;
+    double F[D][D], R[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) F[i][j] = gu[q][i][j] + (i == j ? 1.0 : 0.0);
+    const double J = det<D>(F);
+    if (!(J > 0.0))
+      atomicCAS(reinterpret_cast<unsigned long long*>(a.status), 0ull,
+                (unsigned long long)(a.cell_of_facet[f] + 1));
+    inv<D>(F, R, J);
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < D; ++m) {
+        Fi[q][m][i] = R[m][i];
+        acc = fma(R[m][i], a.normal[(f * nq + q) * D + m], acc);
+      }
+      Fin[q][i] = acc;
+    }
+    coef[q] = -a.k * a.theta * a.mu_f * J * a.dS[f * nq + q];
+  }
+  __syncthreads();
+  for (int t = tid; t < nq * NB * D; t += blockDim.x) {
+    const int q = t / (NB * D), b = (t / D) % NB, i = t % D;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < D; ++m) acc = fma(Fi[q][m][i], Gs[q][b][m], acc);
+    T[q][b][i] = acc;
+  }
+  __syncthreads();
+  double* o = out + f * (int64_t)(NB * NB * D * D);
+  for (int t = tid; t < NB * NB * D * D; t += blockDim.x) {
+    const int b = t / (NB * D * D), aa = (t / (D * D)) % NB, i = (t / D) % D, j = t % D;
+    double acc = 0.0;
+    for (int q = 0; q < nq; ++q) acc = fma(coef[q] * Ns[q][b], T[q][aa][i] * Fin[q][j], acc);
+    o[t] = acc;
+  }
+}
+
+// data[slot u](1+i, 1+j) += sum of the facet blocks mapped to u, in
+// ascending (facet, b, a) order: the order of the reference's np.add.at.
+__global__ void outflow_reduce_kernel(double* data, int nc, int64_t n_unique, const int64_t* slots,
+                                      const int64_t* uptr, const int64_t* contrib,
+                                      const double* local) {
+  const int d = nc - 1, dd = d * d;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_unique * dd) return;
+  const int64_t uu = t / dd;
+  const int ij = (int)(t - uu * dd), i = ij / d, j = ij - (ij / d) * d;
+  double acc = 0.0;
+  for (int64_t e = uptr[uu]; e < uptr[uu + 1]; ++e) acc += local[contrib[e] * dd + ij];
+  data[slots[uu] * nc * nc + (1 + i) * nc + 1 + j] += acc;
+}
+
 // data[slot] += vals (unique slots; host-reduced facet contributions)
 __global__ void add_blocks_kernel(double* data, int bs, int64_t n, const int64_t* slots,
                                   const double* vals) {
@@ -677,6 +765,17 @@ void launch_residual_cells(const ResArgs& a, int dim, int kind, const int32_t* c
     else if (kind == 2) residual_cells_kernel<2, 2><<<g, 128, 0, s>>>(a, cells, out);
     else residual_cells_kernel<2, 3><<<g, 128, 0, s>>>(a, cells, out);
   }
+}
+
+void launch_outflow(const OutflowArgs& a, int dim, int64_t n_unique, const int64_t* slots,
+                    const int64_t* uptr, const int64_t* contrib, double* local, double* data,
+                    cudaStream_t s) {
+  if (a.n_facets == 0) return;
+  if (dim == 3) outflow_local_kernel<3><<<(unsigned)a.n_facets, 256, 0, s>>>(a, local);
+  else outflow_local_kernel<2><<<(unsigned)a.n_facets, 256, 0, s>>>(a, local);
+  const int64_t n = n_unique * dim * dim;
+  outflow_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(data, dim + 1, n_unique, slots,
+                                                                    uptr, contrib, local);
 }
 
 void launch_add_blocks(double* data, int bs, int64_t n, const int64_t* slots, const double* vals,

@@ -30,6 +30,26 @@ struct ResArgs {
   int ext_volume_scaling = 0;
 };
 
+struct OutflowArgs {
+  int64_t n_facets = 0;
+  int nq = 0;                            // facet quadrature points
+  const int32_t* conn = nullptr;         // (n_facets, 3^d) owner-cell nodes
+  const int64_t* cell_of_facet = nullptr;
+  const double* N = nullptr;             // (n_facets, nq, 3^d)
+  const double* G = nullptr;             // (n_facets, nq, 3^d, d)
+  const double* dS = nullptr;            // (n_facets, nq)
+  const double* normal = nullptr;        // (n_facets, nq, d)
+  const double* U = nullptr;             // (n_nodes, 1 + 2d) state
+  int64_t* status = nullptr;
+  double mu_f = 0, k = 0, theta = 0;
+};
+
+// do-nothing outflow blocks of the Jacobian: per-facet local blocks into
+// `local`, then a fixed-order reduction per unique matrix slot into data
+void launch_outflow(const OutflowArgs& a, int dim, int64_t n_unique, const int64_t* slots,
+                    const int64_t* uptr, const int64_t* contrib, double* local, double* data,
+                    cudaStream_t s);
+
 // cell contributions of the theta residual (kind 0 fluid, 1 solid) or of the
 // explicit previous-state forces (kind 2 fluid, 3 solid), added into out
 void launch_residual_cells(const ResArgs& a, int dim, int kind, const int32_t* cells,

@@ -139,6 +139,12 @@ struct Level {
   DevBuf<int32_t> asm_cell_nodes, asm_group_cells;
   DevBuf<double> asm_coords, asm_U, asm_Up, res_out, asm_extra_vals;
   DevBuf<int64_t> asm_extra_slots;
+  // do-nothing outflow facets assembled on the device
+  int64_t of_nf = 0, of_nu = 0;
+  int of_nq = 0;
+  DevBuf<int32_t> of_conn;
+  DevBuf<int64_t> of_cells, of_slots, of_uptr, of_contrib;
+  DevBuf<double> of_N, of_G, of_dS, of_n, of_local;
   std::vector<int64_t> asm_group_ptr;
   std::vector<int> asm_group_kind;
   int64_t n_lps = 0;
@@ -807,6 +813,25 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
     ++m->kernel_launches;
   }
   CKAPI(cudaGetLastError());
+  if (L.of_nf > 0) {
+    alefsi::OutflowArgs o;
+    o.n_facets = L.of_nf;
+    o.nq = L.of_nq;
+    o.conn = L.of_conn.p;
+    o.cell_of_facet = L.of_cells.p;
+    o.N = L.of_N.p;
+    o.G = L.of_G.p;
+    o.dS = L.of_dS.p;
+    o.normal = L.of_n.p;
+    o.U = L.asm_U.p;
+    o.status = m->status.p;
+    o.mu_f = a.mu_f;
+    o.k = a.k;
+    o.theta = a.theta;
+    alefsi::launch_outflow(o, L.dim, L.of_nu, L.of_slots.p, L.of_uptr.p, L.of_contrib.p,
+                           L.of_local.p, L.data.p, s);
+    m->kernel_launches += 2;
+  }
   if (n_extra > 0) {
     CKAPI(L.asm_extra_slots.upload(extra_slots, n_extra, s));
     CKAPI(L.asm_extra_vals.upload(extra_vals, (size_t)n_extra * nc * nc, s));
@@ -826,6 +851,40 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
                                          std::to_string(st - 1));
   m->factorized = false;
   m->graph_valid = false;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_asm_outflow(alefsi_mg h, int32_t level, int64_t n_facets, int32_t nq,
+                          const int32_t* conn, const int64_t* cells, const double* N,
+                          const double* G, const double* dS, const double* normal,
+                          int64_t n_unique, const int64_t* slots, const int64_t* uptr,
+                          const int64_t* contrib) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (!L.has_asm) return fail(ALEFSI_ERR_STATE, "asm_setup missing");
+  const int d = L.dim, nb = d == 2 ? 9 : 27;
+  if (n_facets < 0 || n_unique < 0 || nq < 1 || nq > (d == 2 ? 3 : 9))
+    return fail(ALEFSI_ERR_ARG, "bad outflow facet sizes");
+  cudaStream_t s = m->stream;
+  const size_t nfq = (size_t)n_facets * nq;
+  CKAPI(L.of_conn.upload(conn, (size_t)n_facets * nb, s));
+  CKAPI(L.of_cells.upload(cells, (size_t)n_facets, s));
+  CKAPI(L.of_N.upload(N, nfq * nb, s));
+  CKAPI(L.of_G.upload(G, nfq * nb * d, s));
+  CKAPI(L.of_dS.upload(dS, nfq, s));
+  CKAPI(L.of_n.upload(normal, nfq * d, s));
+  CKAPI(L.of_slots.upload(slots, (size_t)n_unique, s));
+  CKAPI(L.of_uptr.upload(uptr, (size_t)n_unique + 1, s));
+  CKAPI(L.of_contrib.upload(contrib, (size_t)n_facets * nb * nb, s));
+  CKAPI(L.of_local.ensure((size_t)n_facets * nb * nb * d * d));
+  CKAPI(cudaStreamSynchronize(s));
+  L.of_nf = n_facets;
+  L.of_nq = nq;
+  L.of_nu = n_unique;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }

@@ -72,6 +72,7 @@ class DeviceMgSolver:
             _lib.call("alefsi_mg_set_stream", h, C.c_void_p(int(stream)))
         self.ndofs = []
         self._groups = {}
+        self._device_outflow = set()     # levels whose outflow blocks are assembled on device
         for l, lv in enumerate(levels):
             self._set_level(l, lv)
         _lib.call("alefsi_mg_use_graph", h, 1 if use_graph else 0)
@@ -275,6 +276,23 @@ class DeviceMgSolver:
         _lib.call("alefsi_mg_asm_tables", self._h, d, t.N.shape[0],
                   np.ascontiguousarray(t.N), np.ascontiguousarray(t.dN),
                   np.ascontiguousarray(lvl.quad_weights))
+        fq = lvl.outflow
+        if fq is not None and len(fq.cells):
+            # slot reduction plan in np.add.at order (model._outflow_blocks)
+            from . import fem
+            sl = fem.pattern_slots(p.indptr, p.indices, fq.conn).reshape(-1)
+            uniq, inv = np.unique(sl, return_inverse=True)
+            contrib = np.argsort(inv, kind="stable").astype(np.int64)
+            uptr = np.concatenate([[0], np.cumsum(np.bincount(inv, minlength=len(uniq)))])
+            _lib.call("alefsi_mg_asm_outflow", self._h, level, len(fq.cells), fq.N.shape[1],
+                      np.ascontiguousarray(fq.conn, dtype=np.int32),
+                      np.ascontiguousarray(fq.cells, dtype=np.int64),
+                      np.ascontiguousarray(fq.N, dtype=np.float64),
+                      np.ascontiguousarray(fq.G, dtype=np.float64),
+                      np.ascontiguousarray(fq.dS, dtype=np.float64),
+                      np.ascontiguousarray(fq.normal, dtype=np.float64), len(uniq),
+                      np.ascontiguousarray(uniq, dtype=np.int64), uptr.astype(np.int64), contrib)
+            self._device_outflow.add(level)
 
     def asm_momentum(self, level, lvl, mats, k, theta, U, U_prev):
         """Assemble the condensed Jacobian of one level on the device (cells,
@@ -284,7 +302,7 @@ class DeviceMgSolver:
         nc = d + 1
         slots = np.zeros(0, dtype=np.int64)
         vals = np.zeros((0, nc, nc))
-        if lvl.outflow is not None:
+        if lvl.outflow is not None and level not in self._device_outflow:
             with fem.single_blas():
                 local = model._outflow_blocks(lvl.outflow, U, mats, k, theta, d)
             if getattr(lvl, "_outflow_slots", None) is None:    # state independent
