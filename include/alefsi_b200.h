@@ -140,6 +140,18 @@ int alefsi_mg_asm_outflow(alefsi_mg h, int32_t level, int64_t n_facets, int32_t 
  * which = 1. */
 int alefsi_mg_asm_residual(alefsi_mg h, int32_t level, const double* params, const double* U,
                            const double* U_prev, int32_t which, double* out);
+/* Residual tail on the device (reference model.py:191-205 and 277-283):
+ * after this call asm_residual also adds the do-nothing outflow rows
+ * (which = 0: scaled by k*theta into R[:, 1:1+dim]; which = 1: into the
+ * explicit forces) and, for which = 0, k * (L @ p) into R[:, 0] with the
+ * scalar LPS operator L given as CSR (n_nodes rows).  The outflow rows are
+ * reduced per node: onodes (unique facet nodes), and per node u the flat
+ * (facet, b) indices ocontrib[ouptr[u]:ouptr[u+1]] in ascending order.
+ * Requires asm_outflow when n_onodes > 0. */
+int alefsi_mg_asm_residual_tables(alefsi_mg h, int32_t level, const int64_t* lps_indptr,
+                                  const int32_t* lps_indices, const double* lps_vals,
+                                  int64_t n_onodes, const int64_t* onodes, const int64_t* ouptr,
+                                  const int64_t* ocontrib);
 /* Copy a level's operator data (blocks, pp entries) to host memory. */
 int alefsi_mg_get_matrix(alefsi_mg h, int32_t level, double* data, double* pp_data);
 

@@ -56,6 +56,7 @@ SIGNATURES = {
     "alefsi_mg_asm_tables": [_p, _i32, _i32, _p, _p, _p],
     "alefsi_mg_asm_momentum": [_p, _i32, _p, _p, _p, _i64, _p, _p],
     "alefsi_mg_asm_outflow": [_p, _i32, _i64, _i32, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p],
+    "alefsi_mg_asm_residual_tables": [_p, _i32, _p, _p, _p, _i64, _p, _p, _p],
     "alefsi_mg_get_matrix": [_p, _i32, _p, _p],
     "alefsi_mg_asm_residual": [_p, _i32, _p, _p, _p, _i32, _p],
     "alefsi_mg_profile": [_p, _i32],

@@ -680,6 +680,104 @@ __global__ void outflow_reduce_kernel(double* data, int nc, int64_t n_unique, co
   data[slots[uu] * nc * nc + (1 + i) * nc + 1 + j] += acc;
 }
 
+// Do-nothing outflow correction of the residual (reference model.py:191-205):
+// per facet, local[b][i] = sum_q dS_q N_qb (-scale mu_f J_q t_qi),
+//   t = F^-T grad(v)^T F^-T n  at the facet points.
+template <int D>
+__global__ void __launch_bounds__(256) outflow_residual_kernel(OutflowArgs a, double scale,
+                                                               double* out) {
+  constexpr int NB = D == 2 ? 9 : 27, NF = 1 + 2 * D, MQ = D == 2 ? 3 : 9;
+  __shared__ double uv[NB][2 * D], Gs[MQ][NB][D], Ns[MQ][NB], val[MQ][D];
+  __shared__ double gvu[MQ][2 * D][D];     // rows 0..D-1 grad v, D..2D-1 grad u
+  const int64_t f = blockIdx.x;
+  const int nq = a.nq, tid = threadIdx.x;
+  for (int t = tid; t < NB * 2 * D; t += blockDim.x) {
+    const int b = t / (2 * D), i = t - b * (2 * D);
+    uv[b][i] = a.U[(int64_t)a.conn[f * NB + b] * NF + 1 + i];
+  }
+  for (int t = tid; t < nq * NB; t += blockDim.x) {
+    const int q = t / NB, b = t - q * NB;
+    Ns[q][b] = a.N[f * nq * NB + t];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Gs[q][b][j] = a.G[(f * nq * NB + t) * D + j];
+  }
+  __syncthreads();
+  for (int t = tid; t < nq * 2 * D * D; t += blockDim.x) {
+    const int q = t / (2 * D * D), i = (t / D) % (2 * D), j = t % D;
+    double acc = 0.0;
+    for (int b = 0; b < NB; ++b) acc = fma(Gs[q][b][j], uv[b][i], acc);
+    gvu[q][i][j] = acc;
+  }
+  __syncthreads();
+  if (tid < nq) {
+    const int q = tid;
+    double F[D][D], R[D][D], A[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) F[i][j] = gvu[q][D + i][j] + (i == j ? 1.0 : 0.0);
+    const double J = det<D>(F);
+    if (!(J > 0.0))
+      atomicCAS(reinterpret_cast<unsigned long long*>(a.status), 0ull,
+                (unsigned long long)(a.cell_of_facet[f] + 1));
+    inv<D>(F, R, J);
+    // A = F^-T grad(v)^T F^-T:  A_ij = sum_{m,l} R_mi gv_lm R_jl
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+          double inner = 0.0;
+#pragma unroll
+          for (int l = 0; l < D; ++l) inner = fma(gvu[q][l][m], R[j][l], inner);
+          acc = fma(R[m][i], inner, acc);
+        }
+        A[i][j] = acc;
+      }
+    const double c = -scale * a.mu_f * J;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) t = fma(A[i][j], a.normal[(f * nq + q) * D + j], t);
+      val[q][i] = c * t * a.dS[f * nq + q];
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < NB * D; t += blockDim.x) {
+    const int b = t / D, i = t - b * D;
+    double acc = 0.0;
+    for (int q = 0; q < nq; ++q) acc = fma(Ns[q][b], val[q][i], acc);
+    out[(f * NB + b) * D + i] = acc;
+  }
+}
+
+// out[node u, off + i] += sum of the facet rows of u, ascending (facet, b)
+__global__ void node_reduce_kernel(int64_t n_unique, int d, const int64_t* nodes,
+                                   const int64_t* uptr, const int64_t* contrib,
+                                   const double* local, double* out, int no, int off) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_unique * d) return;
+  const int64_t u = t / d;
+  const int i = (int)(t - u * d);
+  double acc = 0.0;
+  for (int64_t e = uptr[u]; e < uptr[u + 1]; ++e) acc += local[contrib[e] * d + i];
+  out[nodes[u] * no + off + i] += acc;
+}
+
+// R[:, 0] += k * (L @ p) for the scalar LPS operator (CSR), row per thread
+__global__ void lps_residual_kernel(int64_t n, const int64_t* indptr, const int32_t* indices,
+                                    const double* vals, const double* U, int nf, double k,
+                                    double* out, int no) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double acc = 0.0;
+  for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) acc += vals[e] * U[(int64_t)indices[e] * nf];
+  out[r * no] += k * acc;
+}
+
 // data[slot] += vals (unique slots; host-reduced facet contributions)
 __global__ void add_blocks_kernel(double* data, int bs, int64_t n, const int64_t* slots,
                                   const double* vals) {
@@ -776,6 +874,25 @@ void launch_outflow(const OutflowArgs& a, int dim, int64_t n_unique, const int64
   const int64_t n = n_unique * dim * dim;
   outflow_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(data, dim + 1, n_unique, slots,
                                                                     uptr, contrib, local);
+}
+
+void launch_outflow_residual(const OutflowArgs& a, int dim, double scale, int64_t n_unique,
+                             const int64_t* nodes, const int64_t* uptr, const int64_t* contrib,
+                             double* local, double* out, int no, int off, cudaStream_t s) {
+  if (a.n_facets == 0) return;
+  if (dim == 3) outflow_residual_kernel<3><<<(unsigned)a.n_facets, 256, 0, s>>>(a, scale, local);
+  else outflow_residual_kernel<2><<<(unsigned)a.n_facets, 256, 0, s>>>(a, scale, local);
+  const int64_t n = n_unique * dim;
+  node_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n_unique, dim, nodes, uptr,
+                                                                 contrib, local, out, no, off);
+}
+
+void launch_lps_residual(int64_t n, const int64_t* indptr, const int32_t* indices,
+                         const double* vals, const double* U, int nf, double k, double* out,
+                         int no, cudaStream_t s) {
+  if (n == 0) return;
+  lps_residual_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, indptr, indices, vals, U, nf,
+                                                                  k, out, no);
 }
 
 void launch_add_blocks(double* data, int bs, int64_t n, const int64_t* slots, const double* vals,

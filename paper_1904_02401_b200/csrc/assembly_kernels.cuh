@@ -50,6 +50,16 @@ void launch_outflow(const OutflowArgs& a, int dim, int64_t n_unique, const int64
                     const int64_t* uptr, const int64_t* contrib, double* local, double* data,
                     cudaStream_t s);
 
+// do-nothing outflow term of the residual: per-facet rows into `local`
+// (n_facets, 3^d, d), reduced per node in fixed order into out[:, off:off+d]
+void launch_outflow_residual(const OutflowArgs& a, int dim, double scale, int64_t n_unique,
+                             const int64_t* nodes, const int64_t* uptr, const int64_t* contrib,
+                             double* local, double* out, int no, int off, cudaStream_t s);
+// out[:, 0] += k * (L @ U[:, 0]) for the scalar LPS operator L (CSR)
+void launch_lps_residual(int64_t n, const int64_t* indptr, const int32_t* indices,
+                         const double* vals, const double* U, int nf, double k, double* out,
+                         int no, cudaStream_t s);
+
 // cell contributions of the theta residual (kind 0 fluid, 1 solid) or of the
 // explicit previous-state forces (kind 2 fluid, 3 solid), added into out
 void launch_residual_cells(const ResArgs& a, int dim, int kind, const int32_t* cells,

@@ -145,6 +145,12 @@ struct Level {
   DevBuf<int32_t> of_conn;
   DevBuf<int64_t> of_cells, of_slots, of_uptr, of_contrib;
   DevBuf<double> of_N, of_G, of_dS, of_n, of_local;
+  // residual tail on the device: outflow rows reduced per node, LPS operator
+  bool rt_ready = false;
+  int64_t rt_nodes_n = 0;
+  DevBuf<int64_t> rt_nodes, rt_uptr, rt_contrib, lps_indptr;
+  DevBuf<int32_t> lps_indices;
+  DevBuf<double> lps_vals, rt_local;
   std::vector<int64_t> asm_group_ptr;
   std::vector<int> asm_group_kind;
   int64_t n_lps = 0;
@@ -889,6 +895,36 @@ int alefsi_mg_asm_outflow(alefsi_mg h, int32_t level, int64_t n_facets, int32_t 
   ALEFSI_TRY_END
 }
 
+int alefsi_mg_asm_residual_tables(alefsi_mg h, int32_t level, const int64_t* lps_indptr,
+                                  const int32_t* lps_indices, const double* lps_vals,
+                                  int64_t n_onodes, const int64_t* onodes, const int64_t* ouptr,
+                                  const int64_t* ocontrib) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (!L.has_asm) return fail(ALEFSI_ERR_STATE, "asm_setup missing");
+  const int d = L.dim, nb = d == 2 ? 9 : 27;
+  if (n_onodes > 0 && L.of_nf == 0) return fail(ALEFSI_ERR_STATE, "asm_outflow missing");
+  cudaStream_t s = m->stream;
+  const int64_t nnz = lps_indptr[L.n_nodes];
+  CKAPI(L.lps_indptr.upload(lps_indptr, (size_t)L.n_nodes + 1, s));
+  CKAPI(L.lps_indices.upload(lps_indices, (size_t)nnz, s));
+  CKAPI(L.lps_vals.upload(lps_vals, (size_t)nnz, s));
+  if (n_onodes > 0) {
+    CKAPI(L.rt_nodes.upload(onodes, (size_t)n_onodes, s));
+    CKAPI(L.rt_uptr.upload(ouptr, (size_t)n_onodes + 1, s));
+    CKAPI(L.rt_contrib.upload(ocontrib, (size_t)L.of_nf * nb, s));
+    CKAPI(L.rt_local.ensure((size_t)L.of_nf * nb * d));
+  }
+  CKAPI(cudaStreamSynchronize(s));
+  L.rt_nodes_n = n_onodes;
+  L.rt_ready = true;
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
 // params = rho_f, mu_f, rho_s, mu_s, lam_s, k, theta, f0, f1, f2, ext_model
 // (0 harmonic / 1 linear elasticity), ext_mu, ext_lam, ext_volume_scaling.
 // which = 0: cell parts of the theta residual -> out (n_nodes, 1+2d);
@@ -935,6 +971,32 @@ int alefsi_mg_asm_residual(alefsi_mg h, int32_t level, const double* params, con
     const int kind = L.asm_group_kind[g] + (which == 1 ? 2 : 0);
     alefsi::launch_residual_cells(a, d, kind, L.asm_group_cells.p + b, e - b, L.res_out.p, s);
     ++m->kernel_launches;
+  }
+  if (L.rt_ready) {
+    if (L.of_nf > 0) {
+      alefsi::OutflowArgs o;
+      o.n_facets = L.of_nf;
+      o.nq = L.of_nq;
+      o.conn = L.of_conn.p;
+      o.cell_of_facet = L.of_cells.p;
+      o.N = L.of_N.p;
+      o.G = L.of_G.p;
+      o.dS = L.of_dS.p;
+      o.normal = L.of_n.p;
+      o.U = which == 0 ? L.asm_U.p : L.asm_Up.p;
+      o.status = m->status.p;
+      o.mu_f = a.mu_f;
+      const double scale = which == 0 ? a.k * a.theta : 1.0;
+      alefsi::launch_outflow_residual(o, d, scale, L.rt_nodes_n, L.rt_nodes.p, L.rt_uptr.p,
+                                      L.rt_contrib.p, L.rt_local.p, L.res_out.p, no,
+                                      which == 0 ? 1 : 0, s);
+      m->kernel_launches += 2;
+    }
+    if (which == 0) {
+      alefsi::launch_lps_residual(L.n_nodes, L.lps_indptr.p, L.lps_indices.p, L.lps_vals.p,
+                                  L.asm_U.p, nf, a.k, L.res_out.p, no, s);
+      ++m->kernel_launches;
+    }
   }
   CKAPI(cudaGetLastError());
   CKAPI(cudaMemcpyAsync(out, L.res_out.p, sizeof(double) * L.n_nodes * no, cudaMemcpyDeviceToHost, s));

@@ -73,6 +73,7 @@ class DeviceMgSolver:
         self.ndofs = []
         self._groups = {}
         self._device_outflow = set()     # levels whose outflow blocks are assembled on device
+        self._device_tail = set()        # levels whose residual tail runs on device
         for l, lv in enumerate(levels):
             self._set_level(l, lv)
         _lib.call("alefsi_mg_use_graph", h, 1 if use_graph else 0)
@@ -293,6 +294,21 @@ class DeviceMgSolver:
                       np.ascontiguousarray(fq.normal, dtype=np.float64), len(uniq),
                       np.ascontiguousarray(uniq, dtype=np.int64), uptr.astype(np.int64), contrib)
             self._device_outflow.add(level)
+        # residual tail: outflow rows per node (np.add.at order) and LPS CSR
+        L = lvl.lps_csr()
+        onodes = np.zeros(0, dtype=np.int64)
+        ouptr = np.zeros(1, dtype=np.int64)
+        ocontrib = np.zeros(0, dtype=np.int64)
+        if level in self._device_outflow:
+            onodes, inv = np.unique(fq.conn.reshape(-1), return_inverse=True)
+            ocontrib = np.argsort(inv, kind="stable").astype(np.int64)
+            ouptr = np.concatenate([[0], np.cumsum(np.bincount(inv, minlength=len(onodes)))])
+        _lib.call("alefsi_mg_asm_residual_tables", self._h, level,
+                  np.ascontiguousarray(L.indptr, dtype=np.int64),
+                  np.ascontiguousarray(L.indices, dtype=np.int32),
+                  np.ascontiguousarray(L.data, dtype=np.float64), len(onodes),
+                  np.ascontiguousarray(onodes, dtype=np.int64), ouptr.astype(np.int64), ocontrib)
+        self._device_tail.add(level)
 
     def asm_momentum(self, level, lvl, mats, k, theta, U, U_prev):
         """Assemble the condensed Jacobian of one level on the device (cells,

@@ -269,12 +269,14 @@ def theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit=None, device=
         if device is None:
             return _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit)
         mg, level = device
-        d = lvl.dim
+        tail = level in getattr(mg, "_device_tail", ())   # outflow + LPS terms on device
         if explicit is None:
             explicit = mg.asm_residual(level, lvl, mats, flags, k, theta, None, U_prev, which=1)
-            outflow_correction(lvl, mats, U_prev, explicit)
+            if not tail:
+                outflow_correction(lvl, mats, U_prev, explicit)
         R = mg.asm_residual(level, lvl, mats, flags, k, theta, U, U_prev, which=0)
-        return _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R), explicit
+        return _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R,
+                              device_tail=tail), explicit
 
 
 def _chunked_scatter(lvl, cells, fn, out, chunk=1024):
@@ -347,16 +349,19 @@ def _theta_residual(lvl, mats, flags, k, theta, U, U_prev, explicit):
     return _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R), explicit
 
 
-def _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R):
+def _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R, device_tail=False):
     """Explicit theta part, outflow correction, LPS, velocity-deformation
-    relation rows and constraint masking (reference model.py:277-292)."""
+    relation rows and constraint masking (reference model.py:277-292).
+    ``device_tail``: the outflow and LPS terms are already in R (added by
+    the device residual)."""
     d = lvl.dim
     n = lvl.n_nodes
     R[:, 1:1 + d] += k * (1.0 - theta) * explicit
-    Xc = np.zeros((n, d))
-    outflow_correction(lvl, mats, U, Xc, scale=k * theta)
-    R[:, 1:1 + d] += Xc
-    R[:, 0] += k * (lvl.lps_csr() @ U[:, 0])
+    if not device_tail:
+        Xc = np.zeros((n, d))
+        outflow_correction(lvl, mats, U, Xc, scale=k * theta)
+        R[:, 1:1 + d] += Xc
+        R[:, 0] += k * (lvl.lps_csr() @ U[:, 0])
     deficit = (U[:, 1 + d:] - U_prev[:, 1 + d:] - k * theta * U[:, 1:1 + d]
                - k * (1.0 - theta) * U_prev[:, 1:1 + d])
     rel = lvl.solid_mass_csr() @ deficit
