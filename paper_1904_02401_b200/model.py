@@ -364,8 +364,7 @@ def _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R, device_tail=Fals
         R[:, 0] += k * (lvl.lps_csr() @ U[:, 0])
     deficit = (U[:, 1 + d:] - U_prev[:, 1 + d:] - k * theta * U[:, 1:1 + d]
                - k * (1.0 - theta) * U_prev[:, 1:1 + d])
-    rel = lvl.solid_mass_csr() @ deficit
-    R[lvl.relation_nodes, 1 + d:] = rel[lvl.relation_nodes]
+    R[lvl.relation_nodes, 1 + d:] = lvl.solid_mass_rows() @ deficit
     R[lvl.residual_zero_mask] = 0.0
     return R
 

@@ -205,12 +205,7 @@ def solve_reduced_linear(problem, stack, R, U, U_prev, k, theta):
     g = np.zeros((n, d))
     g[lvl.interface_nodes] = du[lvl.interface_nodes]
     if "interface_csr" not in blocks:
-        # g vanishes off the interface: only those columns of the extension
-        # operator contribute (same terms, same order, a fraction of the work)
-        cols = np.sort((np.asarray(lvl.interface_nodes)[:, None] * d + np.arange(d)).reshape(-1))
-        sub = blocks["raw_csr"][:, cols].tocsr()
-        sub.sort_indices()
-        blocks["interface_csr"] = (cols, sub)
+        blocks["interface_csr"] = interface_columns(blocks["raw"], lvl.interface_nodes, d)
     cols, sub = blocks["interface_csr"]
     rhs = -R[:, 1 + d:] / k - (sub @ g.reshape(-1)[cols]).reshape(n, d)
     rhs[lvl.ext_dirichlet] = 0.0
@@ -222,6 +217,32 @@ def solve_reduced_linear(problem, stack, R, U, U_prev, k, theta):
     W[rel, 1 + d:] = du[rel]
     W[lvl.u_dirichlet_nodes, 1 + d:] = 0.0
     return W, mom_stats, ext_stats
+
+
+def interface_columns(raw, interface_nodes, d):
+    """(cols, sub): the columns ``cols`` (interface node dofs, ascending) of
+    the raw extension operator as a scalar CSR, built from the blocks whose
+    column node is on the interface.  The lifting term ``g`` vanishes off the
+    interface, so ``sub @ g[cols]`` equals the reference's full product row by
+    row: same nonzeros, ascending columns, no explicit zeros."""
+    import scipy.sparse as sp
+    p = raw.pattern
+    nodes = np.sort(np.asarray(interface_nodes))
+    cols = (nodes[:, None] * d + np.arange(d)).reshape(-1)
+    rank = np.full(p.n_nodes, -1, dtype=np.int64)
+    rank[nodes] = np.arange(len(nodes))
+    blk_col = rank[p.indices]
+    sel = np.flatnonzero(blk_col >= 0)
+    blk_row = np.repeat(np.arange(p.n_nodes), np.diff(p.indptr))[sel]
+    a = np.arange(d)
+    rows = (blk_row[:, None, None] * d + a[None, :, None]) + 0 * a[None, None, :]
+    cc = (blk_col[sel][:, None, None] * d + a[None, None, :]) + 0 * a[None, :, None]
+    sub = sp.csr_matrix((raw.data[sel].reshape(-1), (rows.reshape(-1), cc.reshape(-1))),
+                        shape=(p.n_nodes * d, len(cols)))
+    sub.sum_duplicates()
+    sub.eliminate_zeros()
+    sub.sort_indices()
+    return cols, sub
 
 
 def line_search(residual_of, U, W, res_norm, max_halvings=4):

@@ -140,3 +140,34 @@ def test_live_reference_mesh_entities_3d():
             assert np.array_equal(ma.facets[lab], mb.facets[lab])
             assert np.array_equal(ma.facet_cells[lab], mb.facet_cells[lab])
             assert np.array_equal(ma.boundary_nodes[lab], mb.boundary_nodes[lab])
+
+
+@pytest.mark.parametrize("name", ["2d_mini", "3d_tiny"])
+def test_interface_columns_match_full_product(name):
+    """The extension lifting uses only the interface columns of the raw
+    extension operator: same CSR (values, order) as slicing the full scalar
+    operator, bitwise-equal products."""
+    from paper_1904_02401_b200 import newton
+    prob = W.CONFIGS[name].problem()
+    lvl = prob.fine
+    d = lvl.dim
+    raw = prob.extension_blocks(len(prob.levels) - 1)["raw"]
+    cols = np.sort((np.asarray(lvl.interface_nodes)[:, None] * d + np.arange(d)).reshape(-1))
+    ref = raw.to_csr()[:, cols].tocsr()
+    ref.sort_indices()
+    c2, sub = newton.interface_columns(raw, lvl.interface_nodes, d)
+    assert np.array_equal(cols, c2)
+    assert np.array_equal(ref.indptr, sub.indptr) and np.array_equal(ref.indices, sub.indices)
+    assert np.array_equal(ref.data, sub.data)
+    g = np.random.default_rng(1).standard_normal(len(cols))
+    assert np.array_equal(ref @ g, sub @ g)
+
+
+def test_solid_mass_rows_match_full_product():
+    """Residual relation rows from the row-sliced solid mass matrix: bitwise
+    equal to the rows of the full product."""
+    prob = W.CONFIGS["3d_tiny"].problem()
+    lvl = prob.fine
+    x = np.random.default_rng(2).standard_normal((lvl.n_nodes, lvl.dim))
+    full = lvl.solid_mass_csr() @ x
+    assert np.array_equal(full[lvl.relation_nodes], lvl.solid_mass_rows() @ x)
