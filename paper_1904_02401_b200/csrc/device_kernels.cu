@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 #include "device_kernels.cuh"
@@ -39,6 +40,11 @@ __device__ __forceinline__ double block_sum_256(double v, double* red) {
     r = warp_sum(r);
   }
   return r;  // valid in thread 0
+}
+
+// 32-byte quads usable: length and stride multiples of 4, aligned base
+inline bool vec4_ok(const double* p, int64_t ld, int64_t n) {
+  return n % 4 == 0 && ld % 4 == 0 && reinterpret_cast<uintptr_t>(p) % 32 == 0;
 }
 
 inline int grid_for(int64_t n, int per_block) { return (int)((n + per_block - 1) / per_block); }
@@ -738,10 +744,70 @@ __global__ void transfer_kernel(int64_t nrows, int nc, const int64_t* __restrict
   const int64_t row = t / nc;
   const int c = (int)(t - row * nc);
   double acc = 0.0;
-  for (int64_t e = ptr[row]; e < ptr[row + 1]; ++e)
+  const int64_t end = ptr[row + 1];
+  int64_t e = ptr[row];
+  // loads of four entries in flight, sums in stored order (long restriction rows)
+  for (; e + 4 <= end; e += 4) {
+    const double v0 = __ldg(val + e), v1 = __ldg(val + e + 1), v2 = __ldg(val + e + 2),
+                 v3 = __ldg(val + e + 3);
+    const double x0 = __ldg(src + (int64_t)__ldg(idx + e) * nc + c);
+    const double x1 = __ldg(src + (int64_t)__ldg(idx + e + 1) * nc + c);
+    const double x2 = __ldg(src + (int64_t)__ldg(idx + e + 2) * nc + c);
+    const double x3 = __ldg(src + (int64_t)__ldg(idx + e + 3) * nc + c);
+    acc = __dadd_rn(acc, __dmul_rn(v0, x0));
+    acc = __dadd_rn(acc, __dmul_rn(v1, x1));
+    acc = __dadd_rn(acc, __dmul_rn(v2, x2));
+    acc = __dadd_rn(acc, __dmul_rn(v3, x3));
+  }
+  for (; e < end; ++e)
     acc = __dadd_rn(acc, __dmul_rn(__ldg(val + e), __ldg(src + (int64_t)__ldg(idx + e) * nc + c)));
   if (constrained[t]) acc = 0.0;
   dst[t] = add ? __dadd_rn(dst[t], acc) : acc;
+}
+
+// NC = 4: one thread per row applies the row's (val, idx) run to all four
+// components (one 32-byte load of the source block per entry), four entries
+// in flight per step.  Per component the products and sums are those of
+// transfer_kernel in the same order: bitwise identical.
+__global__ void transfer4_kernel(int64_t nrows, const int64_t* __restrict__ ptr,
+                                 const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                 const double* __restrict__ src,
+                                 const uint8_t* __restrict__ constrained,
+                                 double* __restrict__ dst, int add) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  const int64_t beg = ptr[row], end = ptr[row + 1];
+  d4 acc = {0.0, 0.0, 0.0, 0.0};
+  auto step = [&](double v, const d4& x) {
+    acc.x = __dadd_rn(acc.x, __dmul_rn(v, x.x));
+    acc.y = __dadd_rn(acc.y, __dmul_rn(v, x.y));
+    acc.z = __dadd_rn(acc.z, __dmul_rn(v, x.z));
+    acc.w = __dadd_rn(acc.w, __dmul_rn(v, x.w));
+  };
+  int64_t e = beg;
+  for (; e + 4 <= end; e += 4) {
+    const double v0 = __ldg(val + e), v1 = __ldg(val + e + 1), v2 = __ldg(val + e + 2),
+                 v3 = __ldg(val + e + 3);
+    const int c0 = __ldg(idx + e), c1 = __ldg(idx + e + 1), c2 = __ldg(idx + e + 2),
+              c3 = __ldg(idx + e + 3);
+    const d4 x0 = ld256_ro(src + (int64_t)c0 * 4), x1 = ld256_ro(src + (int64_t)c1 * 4);
+    const d4 x2 = ld256_ro(src + (int64_t)c2 * 4), x3 = ld256_ro(src + (int64_t)c3 * 4);
+    step(v0, x0);
+    step(v1, x1);
+    step(v2, x2);
+    step(v3, x3);
+  }
+  for (; e < end; ++e) step(__ldg(val + e), ld256_ro(src + (int64_t)__ldg(idx + e) * 4));
+  const uchar4 m = reinterpret_cast<const uchar4*>(constrained)[row];
+  double2* o = reinterpret_cast<double2*>(dst + row * 4);
+  double2 a = {m.x ? 0.0 : acc.x, m.y ? 0.0 : acc.y}, b = {m.z ? 0.0 : acc.z, m.w ? 0.0 : acc.w};
+  if (add) {
+    const double2 a0 = o[0], b0 = o[1];
+    a = {__dadd_rn(a0.x, a.x), __dadd_rn(a0.y, a.y)};
+    b = {__dadd_rn(b0.x, b.x), __dadd_rn(b0.y, b.y)};
+  }
+  o[0] = a;
+  o[1] = b;
 }
 
 // --------------------------------------------------------------------------
@@ -865,6 +931,11 @@ __global__ void __launch_bounds__(256) dense_matvec_kernel(int64_t n, const doub
 // --------------------------------------------------------------------------
 constexpr int kBatch = 8;
 
+// VW = 4: every thread streams 32-byte quads (one LDG.256 per vector) so
+// that a warp keeps (nvec + 1) KiB in flight per iteration; w.w is folded
+// into the first pass.  VW = 1: scalar path for lengths that are not a
+// multiple of 4 (2D).  Fixed element-to-thread map: deterministic.
+template <int VW>
 __global__ void __launch_bounds__(256) multi_dot_kernel(int nvec, const double* __restrict__ V,
                                                         int64_t ldv, const double* __restrict__ w,
                                                         int64_t n, double* __restrict__ partial,
@@ -874,15 +945,37 @@ __global__ void __launch_bounds__(256) multi_dot_kernel(int nvec, const double* 
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
   const int nout = nvec + 1;
-  for (int j0 = 0; j0 < nvec; j0 += kBatch) {
+  const int64_t nv = n / VW;
+  double sq = 0.0;
+  for (int j0 = 0; j0 < nvec || j0 == 0; j0 += kBatch) {
     double acc[kBatch];
 #pragma unroll
     for (int q = 0; q < kBatch; ++q) acc[q] = 0.0;
-    for (int64_t i = gt; i < n; i += gs) {
-      const double wi = __ldg(w + i);
+    for (int64_t i = gt; i < nv; i += gs) {
+      if constexpr (VW == 4) {
+        const d4 wi = ld256_ro(w + 4 * i);
+        if (j0 == 0) {
+          sq = fma(wi.x, wi.x, sq);
+          sq = fma(wi.y, wi.y, sq);
+          sq = fma(wi.z, wi.z, sq);
+          sq = fma(wi.w, wi.w, sq);
+        }
 #pragma unroll
-      for (int q = 0; q < kBatch; ++q)
-        if (j0 + q < nvec) acc[q] = fma(__ldg(V + (int64_t)(j0 + q) * ldv + i), wi, acc[q]);
+        for (int q = 0; q < kBatch; ++q)
+          if (j0 + q < nvec) {
+            const d4 v = ld256_ro(V + (int64_t)(j0 + q) * ldv + 4 * i);
+            acc[q] = fma(v.x, wi.x, acc[q]);
+            acc[q] = fma(v.y, wi.y, acc[q]);
+            acc[q] = fma(v.z, wi.z, acc[q]);
+            acc[q] = fma(v.w, wi.w, acc[q]);
+          }
+      } else {
+        const double wi = __ldg(w + i);
+        if (j0 == 0) sq = fma(wi, wi, sq);
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q)
+          if (j0 + q < nvec) acc[q] = fma(__ldg(V + (int64_t)(j0 + q) * ldv + i), wi, acc[q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < kBatch; ++q) {
@@ -890,11 +983,6 @@ __global__ void __launch_bounds__(256) multi_dot_kernel(int nvec, const double* 
       const double s = block_sum_256(acc[q], red);
       if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * nout + j0 + q] = s;
     }
-  }
-  double sq = 0.0;
-  for (int64_t i = gt; i < n; i += gs) {
-    const double wi = __ldg(w + i);
-    sq = fma(wi, wi, sq);
   }
   const double s = block_sum_256(sq, red);
   if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * nout + nvec] = s;
@@ -913,6 +1001,7 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(int nout, int nblo
   if (threadIdx.x == 0) out[j] = s;
 }
 
+template <int VW>
 __global__ void __launch_bounds__(256) multi_axpy_kernel(int nvec, const double* __restrict__ V,
                                                          int64_t ldv, const double* __restrict__ h,
                                                          double* __restrict__ w, int64_t n,
@@ -926,12 +1015,39 @@ __global__ void __launch_bounds__(256) multi_axpy_kernel(int nvec, const double*
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
   double sq = 0.0;
-  for (int64_t i = gt; i < n; i += gs) {
-    double acc = 0.0;
-    for (int j = 0; j < nvec; ++j) acc = fma(hs[j], __ldg(V + (int64_t)j * ldv + i), acc);
-    const double wi = w[i] - acc;
-    w[i] = wi;
-    sq = fma(wi, wi, sq);
+  if constexpr (VW == 4) {
+    for (int64_t i = gt; i < n / 4; i += gs) {
+      d4 acc = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+      for (int j = 0; j < nvec; ++j) {
+        const double hj = hs[j];
+        const d4 v = ld256_ro(V + (int64_t)j * ldv + 4 * i);
+        acc.x = fma(hj, v.x, acc.x);
+        acc.y = fma(hj, v.y, acc.y);
+        acc.z = fma(hj, v.z, acc.z);
+        acc.w = fma(hj, v.w, acc.w);
+      }
+      double2* wp = reinterpret_cast<double2*>(w + 4 * i);
+      double2 a = wp[0], b = wp[1];
+      a.x -= acc.x;
+      a.y -= acc.y;
+      b.x -= acc.z;
+      b.y -= acc.w;
+      wp[0] = a;
+      wp[1] = b;
+      sq = fma(a.x, a.x, sq);
+      sq = fma(a.y, a.y, sq);
+      sq = fma(b.x, b.x, sq);
+      sq = fma(b.y, b.y, sq);
+    }
+  } else {
+    for (int64_t i = gt; i < n; i += gs) {
+      double acc = 0.0;
+      for (int j = 0; j < nvec; ++j) acc = fma(hs[j], __ldg(V + (int64_t)j * ldv + i), acc);
+      const double wi = w[i] - acc;
+      w[i] = wi;
+      sq = fma(wi, wi, sq);
+    }
   }
   const double s = block_sum_256(sq, red);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
@@ -1150,9 +1266,20 @@ void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int
                                                            omega, init_zero);
 }
 
+// ALEFSI_TRANSFER4=0 keeps the thread-per-dof transfer kernel (A/B only)
+bool transfer4_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_TRANSFER4");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 void launch_restrict(int64_t n_coarse, int nc, const int64_t* ptr, const int32_t* idx,
                      const double* val, const double* r_fine, const uint8_t* constrained_coarse,
                      double* b_coarse, cudaStream_t s) {
+  // restriction rows are long (a coarse node collects ~100 fine nodes): keep a
+  // thread per (row, component) for parallelism
   transfer_kernel<<<grid_for(n_coarse * nc, 256), 256, 0, s>>>(
       n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
 }
@@ -1160,8 +1287,12 @@ void launch_restrict(int64_t n_coarse, int nc, const int64_t* ptr, const int32_t
 void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_t* idx,
                         const double* val, const double* x_coarse,
                         const uint8_t* constrained_fine, double* x_fine, cudaStream_t s) {
-  transfer_kernel<<<grid_for(n_fine * nc, 256), 256, 0, s>>>(
-      n_fine, nc, ptr, idx, val, x_coarse, constrained_fine, x_fine, 1);
+  if (nc == 4 && vec4_ok(x_coarse, 0, 4) && vec4_ok(x_fine, 0, 4) && transfer4_enabled())
+    transfer4_kernel<<<grid_for(n_fine, 128), 128, 0, s>>>(n_fine, ptr, idx, val, x_coarse,
+                                                           constrained_fine, x_fine, 1);
+  else
+    transfer_kernel<<<grid_for(n_fine * nc, 256), 256, 0, s>>>(
+        n_fine, nc, ptr, idx, val, x_coarse, constrained_fine, x_fine, 1);
 }
 
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s) {
@@ -1187,14 +1318,20 @@ void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
 
 void launch_multi_dot(int nvec, const double* V, int64_t ldv, const double* w, int64_t n,
                       double* partial, double* out, const int* flag, cudaStream_t s) {
-  multi_dot_kernel<<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, w, n, partial, flag);
+  if (vec4_ok(V, ldv, n) && vec4_ok(w, 0, n))
+    multi_dot_kernel<4><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, w, n, partial, flag);
+  else
+    multi_dot_kernel<1><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, w, n, partial, flag);
   reduce_partials_kernel<<<nvec + 1, 256, 0, s>>>(nvec + 1, kRedBlocks, partial, out, flag);
 }
 
 void launch_multi_axpy(int nvec, const double* V, int64_t ldv, const double* h, double* w,
                        int64_t n, double* partial, double* out, const int* flag,
                        cudaStream_t s) {
-  multi_axpy_kernel<<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, h, w, n, partial, flag);
+  if (vec4_ok(V, ldv, n) && vec4_ok(w, 0, n))
+    multi_axpy_kernel<4><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, h, w, n, partial, flag);
+  else
+    multi_axpy_kernel<1><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, h, w, n, partial, flag);
   reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, out, flag);
 }
 

@@ -55,7 +55,9 @@ void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_
                         const uint8_t* constrained_fine, double* x_fine, cudaStream_t s);
 
 // ---- coarse level: dense inverse and apply
+// work: dense_inverse_work(n) doubles
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s);
+inline int64_t dense_inverse_work(int64_t n) { return 2 * n + 2; }
 void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
                          cudaStream_t s);
 

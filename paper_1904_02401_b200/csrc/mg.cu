@@ -414,7 +414,7 @@ struct MgHandle {
       CK(cudaMemsetAsync(coarse_inv.p, 0, sizeof(double) * n0 * n0, stream));
       launch_split_to_dense(C.mat(), coarse_inv.p, stream);
     }
-    CK(coarse_work.ensure(2 * n0 + 2));
+    CK(coarse_work.ensure((size_t)dense_inverse_work(n0)));
     if (dense_inverse(coarse_inv.p, n0, coarse_work.p, status.p, stream) != 0)
       return fail(ALEFSI_ERR_ARG, "coarse level too large for the dense inverse (" +
                                       std::to_string(n0) + " > 4096 dofs)");
