@@ -63,6 +63,15 @@ int alefsi_scatter_add_blocks(int64_t n_nodes, const int64_t* indptr, const int3
 int alefsi_pattern_match(int64_t n_nodes, const int64_t* a_ptr, const int32_t* a_idx,
                          const int64_t* b_ptr, const int32_t* b_idx, int64_t* slot_in_a);
 
+/* Entries of the LPS macro pattern outside the cell pattern (to_cell < 0):
+ * the scalar pressure-extension pattern pp_indptr / pp_indices and, per macro
+ * entry, its extension slot to_pp (-1 when it has a cell slot).  Completes
+ * the split of reference problem.py:79-90 (the LPS operator on the union
+ * pattern) into cell blocks + pressure extension. */
+int alefsi_split_extension(int64_t n_nodes, const int64_t* mptr, const int32_t* mind,
+                           const int64_t* to_cell, int64_t* pp_indptr, int32_t* pp_indices,
+                           int64_t* to_pp);
+
 /* Greedy first-fit patch coloring; replaces color_patches
  * (reference mesh.py:522-556).  patch_size is the dof count per patch. */
 int alefsi_color_patches(int64_t n_patches, const int64_t* patch_ptr, const int64_t* patch_nodes,

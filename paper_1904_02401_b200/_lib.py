@@ -30,6 +30,7 @@ SIGNATURES = {
     "alefsi_scatter_add_blocks": [_i64, _p, _p, _i64, _i32, _p, _i32, _p, _p, _i32],
     "alefsi_color_patches": [_i64, _p, _p, _p, _i64, _p, _p],
     "alefsi_pattern_match": [_i64, _p, _p, _p, _p, _p],
+    "alefsi_split_extension": [_i64, _p, _p, _p, _p, _p, _p],
     # device multigrid hierarchy
     "alefsi_mg_create": [_i32, _i32, _i32, _i32, _f64, _p],
     "alefsi_mg_destroy": [_p],

@@ -175,6 +175,38 @@ int alefsi_pattern_match(int64_t n_nodes, const int64_t* a_ptr, const int32_t* a
   ALEFSI_TRY_END
 }
 
+// Split of the LPS macro pattern against the cell pattern: entries without a
+// cell slot (to_cell < 0) form the pressure-extension pattern, row by row in
+// macro order.  pp_indptr (n+1), pp_indices (count), to_pp (len(mind), -1 for
+// entries that have a cell slot).  Two parallel passes over the rows.
+int alefsi_split_extension(int64_t n_nodes, const int64_t* mptr, const int32_t* mind,
+                           const int64_t* to_cell, int64_t* pp_indptr, int32_t* pp_indices,
+                           int64_t* to_pp) {
+  ALEFSI_TRY_BEGIN
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t r = 0; r < n_nodes; ++r) {
+    int64_t c = 0;
+    for (int64_t s = mptr[r]; s < mptr[r + 1]; ++s) c += to_cell[s] < 0;
+    pp_indptr[r + 1] = c;
+  }
+  pp_indptr[0] = 0;
+  for (int64_t r = 0; r < n_nodes; ++r) pp_indptr[r + 1] += pp_indptr[r];
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t r = 0; r < n_nodes; ++r) {
+    int64_t o = pp_indptr[r];
+    for (int64_t s = mptr[r]; s < mptr[r + 1]; ++s) {
+      if (to_cell[s] < 0) {
+        pp_indices[o] = mind[s];
+        to_pp[s] = o++;
+      } else {
+        to_pp[s] = -1;
+      }
+    }
+  }
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
 // Greedy first-fit coloring, reference mesh.py:522-556: repeated passes over
 // the patches in stored order; in pass c the first unlabeled, unblocked patch
 // fixes the color's patch size, every later unlabeled unblocked patch of that

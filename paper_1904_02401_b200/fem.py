@@ -375,13 +375,15 @@ def build_split_pattern(n_nodes, cell_groups, macro_nodes):
     else:
         mptr, mind = np.zeros(n_nodes + 1, dtype=np.int64), np.zeros(0, dtype=np.int32)
     to_cell = pattern_match(indptr, indices, mptr, mind)
-    extra = to_cell < 0
-    pp_indices = mind[extra].astype(np.int32)
-    cs = np.concatenate([[0], np.cumsum(extra, dtype=np.int64)])
-    pp_indptr = cs[mptr]
-    to_pp = np.full(len(mind), -1, dtype=np.int64)
-    to_pp[extra] = np.arange(int(cs[-1]))
-    return SplitPattern(n_nodes, indptr, indices, pp_indptr.astype(np.int64), pp_indices,
+    # entries outside the cell pattern, row by row (native, two parallel passes)
+    mind = np.ascontiguousarray(mind, dtype=np.int32)
+    pp_indptr = np.zeros(n_nodes + 1, dtype=np.int64)
+    n_extra = int(np.count_nonzero(to_cell < 0))
+    pp_indices = np.empty(n_extra, dtype=np.int32)
+    to_pp = np.empty(len(mind), dtype=np.int64)
+    _lib.call("alefsi_split_extension", n_nodes, np.ascontiguousarray(mptr, dtype=np.int64), mind,
+              to_cell, pp_indptr, pp_indices, to_pp)
+    return SplitPattern(n_nodes, indptr, indices, pp_indptr, pp_indices,
                         mptr, mind, to_cell, to_pp, diag.astype(np.int64))
 
 
