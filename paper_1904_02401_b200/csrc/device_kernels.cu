@@ -329,18 +329,34 @@ struct ApplyShape {
   static constexpr int PPC = BLK / TPP;                    // patches per CTA
 };
 
+// Up to two patch groups of the same shape (the fluid and the solid patches
+// of a level) in one launch: CTAs [0, blocks0) serve group 0, the rest group
+// 1, so the small solid group runs alongside the fluid group instead of as
+// its own latency-bound launch.
+struct ApplyGroups {
+  int64_t n_patches[2];
+  const int32_t* nodes[2];
+  const double* inv[2];
+  double* y[2];
+  int blocks0;
+};
+
 template <int NP, int LD, int NC, int RPT>
 __global__ void __launch_bounds__(ApplyShape<LD, RPT>::BLK) vanka_apply_kernel(
-    int64_t n_patches, const int32_t* __restrict__ nodes, const double* __restrict__ inv,
-    const double* __restrict__ d, double* __restrict__ Y) {
+    ApplyGroups G, const double* __restrict__ d) {
   constexpr int NPN = NP / NC;
   constexpr int TPP = ApplyShape<LD, RPT>::TPP;
   constexpr int PPC = ApplyShape<LD, RPT>::PPC;
   static_assert(PPC >= 1, "patch too large for one CTA");
   static_assert(LD % RPT == 0 && (RPT == 2 || RPT == 4), "row split");
   __shared__ double ds[PPC][LD];
+  const int gi = blockIdx.x >= (unsigned)G.blocks0 ? 1 : 0;
+  const int64_t n_patches = G.n_patches[gi];
+  const int32_t* __restrict__ nodes = G.nodes[gi];
+  const double* __restrict__ inv = G.inv[gi];
+  double* __restrict__ Y = G.y[gi];
   const int sub = threadIdx.x / TPP, t = threadIdx.x % TPP;
-  const int64_t p = (int64_t)blockIdx.x * PPC + sub;
+  const int64_t p = (int64_t)(blockIdx.x - (gi ? G.blocks0 : 0)) * PPC + sub;
   const bool valid = p < n_patches;
   if (valid) {
     for (int j = t; j < NP; j += TPP) {
@@ -1160,6 +1176,15 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
                                             A.pp_indices, A.pp_data, x, b, y);
 }
 
+// ALEFSI_APPLY_MERGE=0 launches every patch group separately (A/B only)
+bool apply_merge_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_APPLY_MERGE");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 // ALEFSI_APPLY_V4=0 keeps 16-byte column pieces (A/B measurement only)
 bool apply_v4_enabled() {
   static const bool on = [] {
@@ -1170,20 +1195,35 @@ bool apply_v4_enabled() {
 }
 
 template <int NP, int LD, int NC>
-void apply_dispatch(const DevPatchGroup& g, const double* d, double* Y, cudaStream_t s) {
-  double* y = Y + g.y_offset;
+void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, cudaStream_t s) {
+  bool v4 = false;
   if constexpr (LD % 4 == 0) {
-    if (apply_v4_enabled() && reinterpret_cast<uintptr_t>(g.inv) % 32 == 0 &&
-        reinterpret_cast<uintptr_t>(y) % 32 == 0) {
-      const int grid = grid_for(g.n_patches, ApplyShape<LD, 4>::PPC);
-      vanka_apply_kernel<NP, LD, NC, 4>
-          <<<grid, ApplyShape<LD, 4>::BLK, 0, s>>>(g.n_patches, g.nodes, g.inv, d, y);
+    v4 = apply_v4_enabled();
+    for (int i = 0; i < ng; ++i)
+      v4 = v4 && reinterpret_cast<uintptr_t>(g[i].inv) % 32 == 0 &&
+           reinterpret_cast<uintptr_t>(Y + g[i].y_offset) % 32 == 0;
+  }
+  ApplyGroups G{};
+  const int ppc = v4 ? ApplyShape<LD, 4>::PPC : ApplyShape<LD, 2>::PPC;
+  int grid = 0;
+  for (int i = 0; i < 2; ++i) {
+    const DevPatchGroup& gg = g[i < ng ? i : 0];
+    G.n_patches[i] = i < ng ? gg.n_patches : 0;
+    G.nodes[i] = gg.nodes;
+    G.inv[i] = gg.inv;
+    G.y[i] = Y + gg.y_offset;
+    const int b = i < ng ? grid_for(gg.n_patches, ppc) : 0;
+    if (i == 0) G.blocks0 = b;
+    grid += b;
+  }
+  if (grid == 0) return;
+  if constexpr (LD % 4 == 0) {
+    if (v4) {
+      vanka_apply_kernel<NP, LD, NC, 4><<<grid, ApplyShape<LD, 4>::BLK, 0, s>>>(G, d);
       return;
     }
   }
-  const int grid = grid_for(g.n_patches, ApplyShape<LD, 2>::PPC);
-  vanka_apply_kernel<NP, LD, NC, 2>
-      <<<grid, ApplyShape<LD, 2>::BLK, 0, s>>>(g.n_patches, g.nodes, g.inv, d, y);
+  vanka_apply_kernel<NP, LD, NC, 2><<<grid, ApplyShape<LD, 2>::BLK, 0, s>>>(G, d);
 }
 
 // batched global-memory Gauss-Jordan for large patches (see big_* kernels)
@@ -1246,15 +1286,29 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
   else if (A.nc == 4 && g.np == 500) factorize_big(A, g, status, s);
 }
 
-void launch_vanka_apply(const DevPatchGroup& g, int nc, const double* d, double* Y,
-                        cudaStream_t s) {
-  if (g.n_patches == 0) return;
-  if (nc == 3 && g.np == 27) apply_dispatch<27, 28, 3>(g, d, Y, s);
-  else if (nc == 3 && g.np == 75) apply_dispatch<75, 76, 3>(g, d, Y, s);
-  else if (nc == 4 && g.np == 108) apply_dispatch<108, 108, 4>(g, d, Y, s);
-  else if (nc == 2 && g.np == 18) apply_dispatch<18, 18, 2>(g, d, Y, s);
-  else if (nc == 3 && g.np == 81) apply_dispatch<81, 82, 3>(g, d, Y, s);
-  else if (nc == 4 && g.np == 500) apply_dispatch<500, 500, 4>(g, d, Y, s);
+// one launch per pair of consecutive groups with the same patch size;
+// returns the number of launches
+int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const double* d,
+                       double* Y, cudaStream_t s) {
+  int launches = 0;
+  for (int i = 0; i < n_groups;) {
+    const DevPatchGroup& g = groups[i];
+    const int ng = (i + 1 < n_groups && groups[i + 1].np == g.np && groups[i + 1].ld == g.ld &&
+                    apply_merge_enabled())
+                       ? 2 : 1;
+    const DevPatchGroup* gp = groups + i;
+    i += ng;
+    if (g.n_patches == 0 && (ng == 1 || gp[1].n_patches == 0)) continue;
+    if (nc == 3 && g.np == 27) apply_dispatch<27, 28, 3>(gp, ng, d, Y, s);
+    else if (nc == 3 && g.np == 75) apply_dispatch<75, 76, 3>(gp, ng, d, Y, s);
+    else if (nc == 4 && g.np == 108) apply_dispatch<108, 108, 4>(gp, ng, d, Y, s);
+    else if (nc == 2 && g.np == 18) apply_dispatch<18, 18, 2>(gp, ng, d, Y, s);
+    else if (nc == 3 && g.np == 81) apply_dispatch<81, 82, 3>(gp, ng, d, Y, s);
+    else if (nc == 4 && g.np == 500) apply_dispatch<500, 500, 4>(gp, ng, d, Y, s);
+    else continue;
+    ++launches;
+  }
+  return launches;
 }
 
 void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int64_t* goff,

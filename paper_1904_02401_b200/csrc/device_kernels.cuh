@@ -38,9 +38,10 @@ bool vanka_supported(int nc, int np);
 // singular patches set *status to 1 + patch index (first one wins)
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                             cudaStream_t s);
-// Y[p] = A_p^{-1} d[dofs_p]
-void launch_vanka_apply(const DevPatchGroup& g, int nc, const double* d, double* Y,
-                        cudaStream_t s);
+// Y[p] = A_p^{-1} d[dofs_p] for every patch of the groups (consecutive groups
+// of one patch size share a launch); returns the number of launches
+int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const double* d,
+                       double* Y, cudaStream_t s);
 // x[dof] = (init_zero ? 0 : x[dof]) + omega * sum_{p ∋ dof} w[node] * Y[p, dof]
 void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int64_t* goff,
                          const double* weight, const double* Y, double* x, double omega,

@@ -266,19 +266,22 @@ struct MgHandle {
       ++kernel_launches;
       d = L.d.p;
     }
-    for (auto& g : L.groups) {
-      DevPatchGroup dg;
-      dg.npn = g->npn;
-      dg.np = g->np;
-      dg.ld = g->ld;
-      dg.n_patches = g->n_patches;
-      dg.nodes = g->nodes.p;
-      dg.inv = g->inv.p;
-      dg.y_offset = g->y_offset;
+    {
+      std::vector<DevPatchGroup> dg(L.groups.size());
+      const int ng = (int)dg.size();
+      for (int i = 0; i < ng; ++i) {
+        const auto& g = L.groups[i];
+        dg[i].npn = g->npn;
+        dg[i].np = g->np;
+        dg[i].ld = g->ld;
+        dg[i].n_patches = g->n_patches;
+        dg[i].nodes = g->nodes.p;
+        dg[i].inv = g->inv.p;
+        dg[i].y_offset = g->y_offset;
+      }
       int pr = prof_begin(1, l);
-      launch_vanka_apply(dg, L.nc, d, L.Y.p, stream);
+      kernel_launches += launch_vanka_apply(dg.data(), ng, L.nc, d, L.Y.p, stream);
       prof_end(pr);
-      ++kernel_launches;
     }
     int pr = prof_begin(2, l);
     launch_vanka_gather(L.n_nodes, L.nc, L.gptr.p, L.goff.p, L.weight.p, L.Y.p, x, omega,
