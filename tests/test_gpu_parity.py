@@ -200,9 +200,9 @@ def test_device_full_size_vs_reference_history(name):
     np.testing.assert_allclose(vector_checksums(x), g["x_checksums"], rtol=1e-9)
 
 
-@pytest.mark.parametrize("name", ["3d_large"])
+@pytest.mark.parametrize("name", ["3d_large", "2d_large"])
 def test_device_full_size_vs_oracle_history(name):
-    """The headline 4.3M-dof solve against the CPU oracle's full-size run
+    """The headline 4.3M-dof solve (and the 3.2M-dof 2D config 1) against the CPU oracle's full-size run
     (tests/golden/make_oracle_golden.py; the oracle is pinned to the
     reference on every size the reference can run here)."""
     if not os.path.exists(os.path.join(GOLDEN, f"{name}_oracle.json")):
