@@ -914,6 +914,189 @@ __global__ void gj_eliminate_kernel(double* M, int64_t n, int64_t k, const doubl
   }
 }
 
+// Blocked Gauss-Jordan: panels of nb pivot columns.  The panel kernel (one
+// CTA, the n x nb panel in shared memory) runs the nb pivot steps of the
+// unblocked algorithm on the panel only (same pivot choice: largest |value|
+// among rows >= k, lowest row on ties), records the composed row
+// permutation src[] and snapshots the rows it moved or pivots on.  The
+// update kernel then applies the whole panel to the other columns as one
+// rank-nb product:
+//   rows k0..k0+nb-1 :  M[i, j] = sum_s X[i, s] * M_old[src(k0+s), j]   (X = A^-1)
+//   other rows       :  M[i, j] = M_old[src(i), j] + sum_s L[i, s] * M_old[src(k0+s), j]
+// (L = -B A^-1; both stored in the panel columns), i.e. nb pivot steps per
+// pass over the matrix instead of one.
+template <int KB>
+__global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0, int kb,
+                                                        int64_t* perm, int* src_out,
+                                                        double* slab, int* rowslot,
+                                                        int64_t* status) {
+  extern __shared__ __align__(16) unsigned char gj_smem[];
+  double* P = reinterpret_cast<double*>(gj_smem);        // column-major: P[t * n + i]
+  int* src = reinterpret_cast<int*>(P + (size_t)n * kb);  // n
+  __shared__ double sb[32];
+  __shared__ int si[32];
+  __shared__ int s_pr, s_stop, s_ntouch;
+  __shared__ int touched[64], srows[64];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (*status != 0) return;   // an earlier panel hit a zero pivot
+  for (int e = tid; e < n * kb; e += nt) {
+    const int i = e / kb, t = e - i * kb;
+    P[t * n + i] = M[(int64_t)i * n + k0 + t];
+  }
+  for (int i = tid; i < n; i += nt) src[i] = i;
+  if (tid == 0) { s_stop = 0; s_ntouch = 0; }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < KB; ++t) {
+    if (t >= kb) break;
+    const int k = k0 + t;
+    double* Pt = P + t * n;
+    double best = -1.0;
+    int bi = k;
+    for (int i = k + tid; i < n; i += nt) {
+      const double v = fabs(Pt[i]);
+      if (v > best) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if ((tid & 31) == 0) { sb[tid >> 5] = best; si[tid >> 5] = bi; }
+    __syncthreads();
+    if (tid < 32) {
+      best = tid < (nt >> 5) ? sb[tid] : -2.0;
+      bi = tid < (nt >> 5) ? si[tid] : n;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        const int pr = bi < n ? bi : k;
+        s_pr = pr;
+        perm[k] = pr;
+        if (Pt[pr] == 0.0) {
+          s_stop = 1;
+          if (*status == 0) *status = k + 1;
+        }
+        if (s_ntouch < 64) touched[s_ntouch++] = k;
+        if (pr != k && s_ntouch < 64) touched[s_ntouch++] = pr;
+        const int a = src[k];
+        src[k] = src[pr];
+        src[pr] = a;
+      }
+    }
+    __syncthreads();
+    if (s_stop) return;
+    const int pr = s_pr;
+    // pivot row (old row pr) and old row k, read before anyone writes
+    double piv[KB], rk[KB];
+#pragma unroll
+    for (int s2 = 0; s2 < KB; ++s2) {
+      piv[s2] = s2 < kb ? P[s2 * n + pr] : 0.0;
+      rk[s2] = s2 < kb ? P[s2 * n + k] : 0.0;
+    }
+    const double rp = 1.0 / piv[t];
+    __syncthreads();
+    // rows after the swap: row k <- old row pr (scaled), row pr <- old row k;
+    // one thread per row, reading its multiplier before writing the row
+    for (int i = tid; i < n; i += nt) {
+      if (i == k) {
+#pragma unroll
+        for (int s2 = 0; s2 < KB; ++s2)
+          if (s2 < kb) P[s2 * n + k] = (s2 == t) ? rp : piv[s2] * rp;
+        continue;
+      }
+      double row[KB];
+#pragma unroll
+      for (int s2 = 0; s2 < KB; ++s2) row[s2] = s2 < kb ? (i == pr ? rk[s2] : P[s2 * n + i]) : 0.0;
+      const double f = row[t];
+#pragma unroll
+      for (int s2 = 0; s2 < KB; ++s2)
+        if (s2 < kb) P[s2 * n + i] = (s2 == t) ? -f * rp : row[s2] - f * (piv[s2] * rp);
+    }
+    __syncthreads();
+  }
+  // panel columns in their final form
+  for (int e = tid; e < n * kb; e += nt) {
+    const int i = e / kb, t = e - i * kb;
+    M[(int64_t)i * n + k0 + t] = P[t * n + i];
+  }
+  for (int i = tid; i < n; i += nt) {
+    src_out[i] = src[i];
+    rowslot[i] = -1;
+  }
+  __syncthreads();
+  // rows read through the permutation: sources of the pivot positions and of
+  // every moved row, snapshot before the update kernel overwrites them
+  if (tid == 0) {
+    int q = 0;
+    for (int a = 0; a < s_ntouch; ++a) {
+      const int r = src[touched[a]];
+      bool seen = false;
+      for (int c = 0; c < q; ++c) seen = seen || srows[c] == r;
+      if (!seen) {
+        rowslot[r] = q;
+        srows[q++] = r;
+      }
+    }
+    s_ntouch = q;
+  }
+  __syncthreads();
+  const int ncopy = s_ntouch * n;
+  for (int e = tid; e < ncopy; e += nt) {
+    const int q = e / n, j = e - q * n;
+    slab[e] = M[(int64_t)srows[q] * n + j];
+  }
+}
+
+// rank-kb application of a factorised panel to the other columns (see
+// gj_panel_kernel).  CTA tile: 32 rows x 128 columns, thread = one column x
+// 16 rows (coalesced row segments); the tile's permutation sources, panel
+// coefficients and pivot-row segments are staged in shared memory.
+__global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0, int kb,
+                                                        const int* __restrict__ src,
+                                                        const double* __restrict__ slab,
+                                                        const int* __restrict__ rowslot,
+                                                        const int64_t* status) {
+  __shared__ double sK[16][128];
+  __shared__ double cf[32][17];
+  __shared__ int kslot[16], rsrc[32];
+  if (*status != 0) return;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 128, tid = threadIdx.x;
+  if (tid < kb) kslot[tid] = rowslot[src[k0 + tid]];
+  if (tid >= 64 && tid < 96) {
+    const int i = i0 + tid - 64;
+    // -2: pivot position (no base term), -1: unmoved row, else slab row
+    rsrc[tid - 64] = i >= n ? -2 : (i >= k0 && i < k0 + kb) ? -2
+                                 : (src[i] == i ? -1 : rowslot[src[i]]);
+  }
+  for (int e = tid; e < 32 * kb; e += 256) {
+    const int r = e / kb, s2 = e - r * kb, i = i0 + r;
+    cf[r][s2] = i < n ? M[(int64_t)i * n + k0 + s2] : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < kb * 128; e += 256) {
+    const int s2 = e >> 7, jj = e & 127, j = j0 + jj;
+    sK[s2][jj] = j < n ? slab[(int64_t)kslot[s2] * n + j] : 0.0;
+  }
+  __syncthreads();
+  const int jj = tid & 127, j = j0 + jj;
+  if (j >= n || (j >= k0 && j < k0 + kb)) return;
+#pragma unroll 4
+  for (int r = tid >> 7; r < 32; r += 2) {
+    const int i = i0 + r;
+    if (i >= n) break;
+    const int rs = rsrc[r];
+    double acc = rs == -2 ? 0.0 : (rs == -1 ? M[(int64_t)i * n + j] : slab[(int64_t)rs * n + j]);
+    for (int s2 = 0; s2 < kb; ++s2) acc = fma(cf[r][s2], sK[s2][jj], acc);
+    M[(int64_t)i * n + j] = acc;
+  }
+}
+
 __global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1349,7 +1532,59 @@ void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_
         n_fine, nc, ptr, idx, val, x_coarse, constrained_fine, x_fine, 1);
 }
 
+// panel width of the blocked Gauss-Jordan: n x nb panel + n ints in shared memory
+int gj_panel_width(int64_t n) {
+  for (int nb = 16; nb >= 4; nb >>= 1)
+    if (n * nb * 8 + n * 4 <= 225 * 1024 && n >= 4 * nb) return nb;
+  return 0;
+}
+
+// ALEFSI_GJ_BLOCKED=0 keeps the one-pivot-per-launch Gauss-Jordan (A/B only)
+bool gj_blocked_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_GJ_BLOCKED");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s) {
+  const int nb = gj_blocked_enabled() ? gj_panel_width(n) : 0;
+  if (nb > 0 && n <= kGjMaxN) {
+    // work: perm (n int64) | src (n int) | rowslot (n int) | slab (2 nb x n)
+    int64_t* perm = reinterpret_cast<int64_t*>(work);
+    int* src = reinterpret_cast<int*>(work + n);
+    int* rowslot = src + n;
+    double* slab = work + 2 * n;
+    const size_t smem = (size_t)n * nb * 8 + (size_t)n * 4;
+    static bool attr = [] {
+      cudaFuncSetAttribute(gj_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           226 * 1024);
+      cudaFuncSetAttribute(gj_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           226 * 1024);
+      cudaFuncSetAttribute(gj_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           226 * 1024);
+      return true;
+    }();
+    (void)attr;
+    cudaMemsetAsync(status, 0, sizeof(int64_t), s);
+    const dim3 ug((unsigned)grid_for(n, 128), (unsigned)grid_for(n, 32));
+    for (int64_t k0 = 0; k0 < n; k0 += nb) {
+      const int kb = (int)std::min<int64_t>(nb, n - k0);
+      if (nb == 16)
+        gj_panel_kernel<16><<<1, 512, smem, s>>>(M, (int)n, (int)k0, kb, perm, src, slab,
+                                                 rowslot, status);
+      else if (nb == 8)
+        gj_panel_kernel<8><<<1, 512, smem, s>>>(M, (int)n, (int)k0, kb, perm, src, slab,
+                                                rowslot, status);
+      else
+        gj_panel_kernel<4><<<1, 512, smem, s>>>(M, (int)n, (int)k0, kb, perm, src, slab,
+                                                rowslot, status);
+      gj_update_kernel<<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot, status);
+    }
+    gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm);
+    return 0;
+  }
   // work: colk (n doubles) | rp (1 double) | perm (n int64)
   double* colk = work;
   double* rp = work + n;
