@@ -381,19 +381,39 @@ def extension_operator(lvl, flags):
     cells = lvl.fluid_cells
     if len(cells) == 0:
         return A
-    with fem.single_blas():
-        wdet, G = lvl.wdet[cells], lvl.G[cells]
+    # Cell Gram products of the basis gradients as batched BLAS matrix
+    # products over the (quadrature point, component) axis (reference
+    # model.py:442-461 writes them as einsums; same terms, BLAS summation
+    # order, ~1e-16 relative)
+    wdet, G = lvl.wdet[cells], lvl.G[cells]
+    nq, nb = G.shape[1], G.shape[2]
+    if flags.extension_model == "harmonic":
+        w = wdet
+    else:
+        scale = lvl.inv_cell_volume[cells] if flags.ext_volume_scaling else np.ones(len(cells))
+        w = wdet * scale[:, None]
+    local = np.empty((len(cells), nb, nb, d, d))
+    chunk = 2048
+
+    def work(s):
+        Gc, wc = G[s:s + chunk], w[s:s + chunk]
+        m = len(Gc)
         if flags.extension_model == "harmonic":
-            gg = np.einsum("cq,cqam,cqbm->cba", wdet, G, G, optimize=True)
-            local = gg[..., None, None] * np.eye(d)
+            X = np.ascontiguousarray(Gc.transpose(0, 2, 1, 3)).reshape(m, nb, nq * d)
+            Y = (Gc * wc[:, :, None, None]).transpose(0, 2, 1, 3).reshape(m, nb, nq * d)
+            gg = np.matmul(Y, X.transpose(0, 2, 1))                       # (c, b, a)
+            local[s:s + m] = gg[..., None, None] * np.eye(d)
         else:
-            scale = lvl.inv_cell_volume[cells] if flags.ext_volume_scaling else np.ones(len(cells))
-            w = wdet * scale[:, None]
-            gg = np.einsum("cq,cqam,cqbm->cba", w, G, G, optimize=True)
-            local = flags.ext_mu * gg[..., None, None] * np.eye(d)
-            local = local + flags.ext_mu * np.einsum("cq,cqai,cqbj->cbaij", w, G, G, optimize=True)
-            local = local + flags.ext_lam * np.einsum("cq,cqaj,cqbi->cbaij", w, G, G, optimize=True)
-        fem.scatter_blocks(p.indptr, p.indices, A.data, lvl.mesh.cell_nodes[cells], local)
+            X = Gc.reshape(m, nq, nb * d)                                  # (q, a i)
+            Y = (Gc * wc[:, :, None, None]).reshape(m, nq, nb * d)         # (q, b j)
+            T1 = np.matmul(Y.transpose(0, 2, 1), X).reshape(m, nb, d, nb, d)
+            T1 = T1.transpose(0, 1, 3, 4, 2)                               # (c, b, a, i, j)
+            gg = np.trace(T1, axis1=3, axis2=4)                            # (c, b, a)
+            local[s:s + m] = (flags.ext_mu * gg[..., None, None] * np.eye(d)
+                              + flags.ext_mu * T1 + flags.ext_lam * np.swapaxes(T1, -1, -2))
+
+    fem.parallel_chunks(work, range(0, len(cells), chunk))
+    fem.scatter_blocks(p.indptr, p.indices, A.data, lvl.mesh.cell_nodes[cells], local)
     return A
 
 
