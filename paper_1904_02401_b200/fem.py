@@ -230,7 +230,16 @@ def lps_local_matrices(mesh, table, qpoints, G, wdet, delta_cell, groups, macro_
 
     The Q2 pressure gradient is projected onto the parent cell's Q1 space
     (constants on single-cell macros) and the fluctuation is penalised with
-    the per-cell weight delta (reference fem.py:306-358)."""
+    the per-cell weight delta (reference fem.py:306-358):
+        out = F^T D F,   F = (I - Q M^-1 Q^T W) Gk,   M = Q^T W Q,
+    with Gk the macro basis gradients at the children's quadrature points.
+    Gk is block sparse (a child touches 27 of the macro's 125 basis
+    functions), so the product is expanded as
+        out = Gk^T D Gk - C - C^T + coef^T (Q^T D Q) coef,
+        coef = M^-1 Q^T W Gk,   C = (Gk^T D Q) coef,
+    with the Gk terms accumulated child by child: ~1.5 M instead of 10 M
+    multiply-adds per 3D macro and no dense (216 x 375) gradient array
+    (same values to ~1e-15 relative)."""
     dim = mesh.dim
     nm, nch = groups.shape
     nb = table.n_basis
@@ -245,6 +254,7 @@ def lps_local_matrices(mesh, table, qpoints, G, wdet, delta_cell, groups, macro_
             q1[j] = _q1_table(0.5 * (qpoints + off), dim)
     n1 = q1.shape[2]
     Q = q1.reshape(nch * nq, n1)                                 # ((j q), i)
+    d = dim
     out = np.empty((nm, nmn, nmn))
 
     def work(s):
@@ -257,21 +267,32 @@ def lps_local_matrices(mesh, table, qpoints, G, wdet, delta_cell, groups, macro_
         loc = np.searchsorted((mn + key).reshape(-1),
                               (child.reshape(m, -1) + key).reshape(-1)).reshape(m, nch, nb)
         loc -= np.arange(m)[:, None, None] * nmn
-        Gm = np.zeros((m, nch, nq, nmn, dim))
-        idx = np.broadcast_to(loc[:, :, None, :], (m, nch, nq, nb))
         Gc = G[g]                                               # (m, nch, nq, nb, d)
-        for i in range(dim):
-            np.put_along_axis(Gm[..., i], idx, Gc[..., i], axis=3)
-        wq = wdet[g].reshape(m, nch * nq)
-        dq = (delta_cell[g][:, :, None] * wdet[g]).reshape(m, nch * nq)
-        Gk = Gm.reshape(m, nch * nq, nmn * dim)
-        M = np.matmul(Q.T[None] * wq[:, None, :], Q[None])                  # (m, i, l)
-        rhs = np.matmul(Q.T[None] * wq[:, None, :], Gk)                     # (m, i, (a d))
-        coef = np.linalg.solve(M, rhs)
-        fluct = (Gk - np.matmul(Q[None], coef)).reshape(m, nch * nq, nmn, dim)
-        F = fluct.transpose(0, 1, 3, 2).reshape(m, nch * nq * dim, nmn)
-        wts = np.repeat(dq, dim, axis=1)
-        out[s:s + m] = np.matmul(np.swapaxes(F * wts[:, :, None], 1, 2), F)
+        wq = wdet[g]                                            # (m, nch, nq)
+        dq = delta_cell[g][:, :, None] * wq
+        M = np.matmul(Q.T[None] * wq.reshape(m, 1, nch * nq), Q[None])       # (m, i, l)
+        K = np.matmul(Q.T[None] * dq.reshape(m, 1, nch * nq), Q[None])
+        R = np.zeros((m, nmn, n1, d))                           # Gk^T W Q
+        H = np.zeros((m, nmn, n1, d))                           # Gk^T D Q
+        A = np.zeros((m, nmn, nmn))                             # Gk^T D Gk
+        mi = np.arange(m)[:, None]
+        for j in range(nch):
+            Gj = Gc[:, j].transpose(0, 2, 1, 3)                 # (m, nb, nq, d)
+            # within one child the positions loc[:, j] are distinct: plain += scatters
+            R[mi, loc[:, j]] += np.einsum("mbqd,mq,qi->mbid", Gj, wq[:, j], q1[j], optimize=True)
+            H[mi, loc[:, j]] += np.einsum("mbqd,mq,qi->mbid", Gj, dq[:, j], q1[j], optimize=True)
+            X = Gj.reshape(m, nb, nq * d)
+            Y = (Gj * dq[:, j][:, None, :, None]).reshape(m, nb, nq * d)
+            A[mi[:, :, None], loc[:, j][:, :, None], loc[:, j][:, None, :]] += \
+                np.matmul(Y, X.transpose(0, 2, 1))
+        coef = np.linalg.solve(M, R.transpose(0, 2, 1, 3).reshape(m, n1, nmn * d))
+        coef4 = coef.reshape(m, n1, nmn, d)
+        C = np.matmul(H.reshape(m, nmn, n1 * d),
+                      coef4.transpose(0, 1, 3, 2).reshape(m, n1 * d, nmn))
+        KC = np.matmul(K, coef).reshape(m, n1, nmn, d)
+        quad = np.matmul(coef4.transpose(0, 2, 1, 3).reshape(m, nmn, n1 * d),
+                         KC.transpose(0, 1, 3, 2).reshape(m, n1 * d, nmn))
+        out[s:s + m] = A - C - np.swapaxes(C, 1, 2) + quad
 
     parallel_chunks(work, range(0, nm, chunk))
     return out
