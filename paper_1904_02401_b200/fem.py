@@ -96,10 +96,9 @@ class ShapeTable:
 
 
 def _jacobian(dN, X):
-    """J[c,q,i,j] = sum_b X[c,b,i] dN[q,b,j]."""
-    # plain (unoptimised) einsum: same summation order as the reference
-    # (fem.py:97), so the geometry is bitwise identical
-    return np.einsum("qbj,cbi->cqij", dN, X)
+    """J[c,q,i,j] = sum_b X[c,b,i] dN[q,b,j] (reference fem.py:97), as a
+    batched matmul X[c]^T @ dN[q] (BLAS order, ~1e-16 from the einsum form)."""
+    return np.matmul(np.swapaxes(X, 1, 2)[:, None], dN[None])
 
 
 def cell_geometry(mesh, table, weights, cells=None, chunk=2048):
@@ -121,7 +120,7 @@ def cell_geometry(mesh, table, weights, cells=None, chunk=2048):
         Jinv = np.linalg.inv(J)
         # G[c,q] = dN[q] @ Jinv[c,q]: batched matmul (the reference's einsum
         # form sums the same three terms; ~1e-16 apart, 5x faster)
-        G[s:s + chunk] = np.matmul(table.dN[None], Jinv)
+        np.matmul(table.dN[None], Jinv, out=G[s:s + chunk])
         wdet[s:s + chunk] = det * weights[None, :]
 
     parallel_chunks(work, range(0, nc, chunk))
