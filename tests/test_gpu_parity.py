@@ -237,3 +237,26 @@ def test_device_headline_size_properties():
     assert float(torch.linalg.norm(lin)) <= 1e-11 * float(torch.linalg.norm(s.dot(b)))
     x2, st2 = s.gmres(b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
     assert torch.equal(x, x2) and st.residuals == st2.residuals
+
+
+@pytest.mark.parametrize("name", ["2d_mini", "3d_tiny"])
+def test_singular_patch_and_coarse_block_are_reported(name):
+    """A node row of zeros makes every patch containing it singular: the
+    factorisation fails with ALEFSI_ERR_SINGULAR (reference linsolve.py:
+    132-133 raises for a singular patch block) instead of producing NaNs;
+    the same row on the coarse level trips the dense inverse's zero pivot."""
+    import copy
+    from paper_1904_02401_b200 import _lib
+    case = get_case(name)
+    wl = W.CONFIGS[name]
+    for level in (len(case.matrices) - 1, 0):
+        levels = case.mg_levels()
+        A = copy.deepcopy(levels[level]["matrix"])
+        p = A.pattern
+        r = p.n_nodes // 2
+        A.data[p.indptr[r]:p.indptr[r + 1]] = 0.0
+        A.pp_data[p.pp_indptr[r]:p.pp_indptr[r + 1]] = 0.0
+        levels[level] = dict(levels[level], matrix=A)
+        with pytest.raises(_lib.NativeError) as exc:
+            device.DeviceMgSolver(levels, nu_pre=wl.nu_pre, nu_post=wl.nu_post, omega=wl.omega)
+        assert exc.value.code == 3, str(exc.value)
