@@ -17,6 +17,8 @@
 
 namespace alefsi {
 
+bool small_level_kernels_enabled();
+
 namespace {
 
 constexpr int kWarp = 32;
@@ -46,6 +48,11 @@ __device__ __forceinline__ double block_sum_256(double v, double* red) {
 inline bool vec4_ok(const double* p, int64_t ld, int64_t n) {
   return n % 4 == 0 && ld % 4 == 0 && reinterpret_cast<uintptr_t>(p) % 32 == 0;
 }
+
+// levels below this many nodes are L2 resident and latency bound
+constexpr int64_t kSmallLevelNodes = 65536;
+// patch launches below this many patches use the column-split apply
+constexpr int64_t kSmallPatchCount = 8192;
 
 inline int grid_for(int64_t n, int per_block) { return (int)((n + per_block - 1) / per_block); }
 
@@ -198,7 +205,13 @@ __device__ __forceinline__ d4 ld256_ro(const double* p) {       // read-only pat
 // NC = 4 with 32-bit offsets: lane = 4*blk + r loads its whole 32-byte block
 // row and the 32-byte x block with one instruction each (half the load
 // instructions of spmv32_kernel; same FMA order, bitwise-equal results).
-template <int MODE, bool SHFL>
+//
+// UNR: the four column steps of a 32-block chunk are unrolled so their loads
+// are in flight together.  Used on small, L2-resident levels, where a
+// warp's chain of dependent L2 round trips (not resident warps) sets the
+// time; the large levels keep one step at a time for 32 registers and full
+// occupancy.  Same FMA order either way: bitwise-equal results.
+template <int MODE, bool SHFL, bool UNR = false>
 __global__ void __launch_bounds__(256) spmv4_v4_kernel(int64_t n, const int64_t* __restrict__ indptr,
                                                        const int32_t* __restrict__ indices,
                                                        const double* __restrict__ data,
@@ -231,7 +244,7 @@ __global__ void __launch_bounds__(256) spmv4_v4_kernel(int64_t n, const int64_t*
   // handed out by shuffle, so the x gather of an iteration waits on L2 only
   if constexpr (SHFL) for (int base = beg; base < end; base += kWarp) {
     const int cidx = base + lane < end ? __ldcs(indices + base + lane) : 0;
-#pragma unroll 1
+#pragma unroll (UNR ? 4 : 1)
     for (int j = 0; j < kWarp / BPI; ++j) {
       const int col = __shfl_sync(0xffffffffu, cidx, j * BPI + sub);
       const int blk = base + j * BPI + sub;
@@ -392,6 +405,66 @@ __global__ void __launch_bounds__(ApplyShape<LD, RPT>::BLK) vanka_apply_kernel(
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(out), "d"(a0), "d"(a1), "d"(a2),
                  "d"(a3)
                  : "memory");
+  }
+}
+
+// Small patch groups (coarse levels): S thread groups per patch split the
+// column range, partial results combined in fixed order through shared
+// memory — a quarter of the dependent load rounds per thread when there are
+// too few patches to fill the GPU.
+template <int NP, int LD, int NC, int RPT, int S>
+__global__ void __launch_bounds__(ApplyShape<LD, RPT>::TPP * S) vanka_apply_split_kernel(
+    ApplyGroups G, const double* __restrict__ d) {
+  constexpr int NPN = NP / NC;
+  constexpr int TPP = ApplyShape<LD, RPT>::TPP;
+  constexpr int CPS = (NP + S - 1) / S;   // columns per split
+  __shared__ double ds[LD];
+  __shared__ double part[S][LD];
+  const int gi = blockIdx.x >= (unsigned)G.blocks0 ? 1 : 0;
+  const int32_t* __restrict__ nodes = G.nodes[gi];
+  const double* __restrict__ inv = G.inv[gi];
+  double* __restrict__ Y = G.y[gi];
+  const int64_t p = (int64_t)(blockIdx.x - (gi ? G.blocks0 : 0));
+  if (p >= G.n_patches[gi]) return;
+  for (int j = threadIdx.x; j < NP; j += TPP * S) {
+    const int a = j / NC, c = j - a * NC;
+    ds[j] = __ldg(d + (int64_t)__ldg(nodes + p * NPN + a) * NC + c);
+  }
+  __syncthreads();
+  const int sp = threadIdx.x / TPP, t = threadIdx.x % TPP;
+  const bool rows_ok = RPT * t < LD;
+  double acc[RPT];
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+  if (rows_ok) {
+    const double* col = inv + p * (int64_t)(NP * LD) + RPT * t;
+    const int j0 = sp * CPS, j1 = min(NP, j0 + CPS);
+#pragma unroll 9
+    for (int j = j0; j < j1; ++j) {
+      const double dj = ds[j];
+      if constexpr (RPT == 4) {
+        const d4 v = ld256_stream(col + j * LD);
+        acc[0] = fma(v.x, dj, acc[0]);
+        acc[1] = fma(v.y, dj, acc[1]);
+        acc[2] = fma(v.z, dj, acc[2]);
+        acc[3] = fma(v.w, dj, acc[3]);
+      } else {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(col + j * LD));
+        acc[0] = fma(v.x, dj, acc[0]);
+        acc[1] = fma(v.y, dj, acc[1]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) part[sp][RPT * t + r] = acc[r];
+  }
+  __syncthreads();
+  if (sp != 0 || !rows_ok) return;
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    double v = part[0][RPT * t + r];
+#pragma unroll
+    for (int q = 1; q < S; ++q) v += part[q][RPT * t + r];
+    Y[p * (int64_t)LD + RPT * t + r] = v;
   }
 }
 
@@ -781,6 +854,33 @@ __global__ void transfer_kernel(int64_t nrows, int nc, const int64_t* __restrict
   dst[t] = add ? __dadd_rn(dst[t], acc) : acc;
 }
 
+// Restriction on small levels: 8 lanes per (coarse node, component), lane k
+// summing entries k, k+8, ... of the row, combined by a fixed xor-shuffle
+// tree (deterministic; a different association than the sequential sum).
+// The long rows (~100 fine nodes per coarse node) otherwise make every
+// thread a chain of dependent L2 round trips.
+__global__ void __launch_bounds__(256) transfer_split_kernel(
+    int64_t nrows, int nc, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+    const double* __restrict__ val, const double* __restrict__ src,
+    const uint8_t* __restrict__ constrained, double* __restrict__ dst, int add) {
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int k = threadIdx.x & 7;
+  const bool live = g < nrows * nc;
+  const int64_t row = live ? g / nc : 0;
+  const int c = live ? (int)(g - row * nc) : 0;
+  double acc = 0.0;
+  if (live) {
+    const int64_t end = ptr[row + 1];
+    for (int64_t e = ptr[row] + k; e < end; e += 8)
+      acc = __dadd_rn(acc, __dmul_rn(__ldg(val + e), __ldg(src + (int64_t)__ldg(idx + e) * nc + c)));
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o, 8));
+  if (!live || k != 0) return;
+  if (constrained[g]) acc = 0.0;
+  dst[g] = add ? __dadd_rn(dst[g], acc) : acc;
+}
+
 // NC = 4: one thread per row applies the row's (val, idx) run to all four
 // components (one 32-byte load of the source block per entry), four entries
 // in flight per step.  Per component the products and sums are those of
@@ -1097,9 +1197,11 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0
   }
 }
 
-__global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm) {
+// (skipped after a zero pivot: the pivot list is then incomplete)
+__global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm,
+                                     const int64_t* status) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || *status != 0) return;
   double* row = M + i * n;
   for (int64_t k = n - 1; k >= 0; --k) {
     const int64_t p = perm[k];
@@ -1335,7 +1437,9 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
                        A.n_nodes * NC < ((int64_t)1 << 31);
     const int var = spmv_variant();
     if (idx32 && NC == 4 && var > 0) {
+      const bool unr = A.n_nodes < kSmallLevelNodes && small_level_kernels_enabled();
       auto k = var == 1 ? (mode == 0 ? spmv4_v4_kernel<0, false> : spmv4_v4_kernel<1, false>)
+               : unr    ? (mode == 0 ? spmv4_v4_kernel<0, true, true> : spmv4_v4_kernel<1, true, true>)
                         : (mode == 0 ? spmv4_v4_kernel<0, true> : spmv4_v4_kernel<1, true>);
       k<<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr, A.pp_indices,
                              A.pp_data, x, b, y);
@@ -1400,6 +1504,21 @@ void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, 
     grid += b;
   }
   if (grid == 0) return;
+  const int64_t total = G.n_patches[0] + G.n_patches[1];
+  if (total < kSmallPatchCount && small_level_kernels_enabled() && NP <= 108) {
+    // one CTA per patch, 4 column splits
+    G.blocks0 = (int)G.n_patches[0];
+    const int sgrid = (int)total;
+    if constexpr (LD % 4 == 0) {
+      if (v4) {
+        vanka_apply_split_kernel<NP, LD, NC, 4, 4>
+            <<<sgrid, ApplyShape<LD, 4>::TPP * 4, 0, s>>>(G, d);
+        return;
+      }
+    }
+    vanka_apply_split_kernel<NP, LD, NC, 2, 4><<<sgrid, ApplyShape<LD, 2>::TPP * 4, 0, s>>>(G, d);
+    return;
+  }
   if constexpr (LD % 4 == 0) {
     if (v4) {
       vanka_apply_kernel<NP, LD, NC, 4><<<grid, ApplyShape<LD, 4>::BLK, 0, s>>>(G, d);
@@ -1503,6 +1622,15 @@ void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int
                                                            omega, init_zero);
 }
 
+// ALEFSI_SMALL_LEVELS=0 keeps the large-level kernels on every level (A/B only)
+bool small_level_kernels_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_SMALL_LEVELS");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 // ALEFSI_TRANSFER4=0 keeps the thread-per-dof transfer kernel (A/B only)
 bool transfer4_enabled() {
   static const bool on = [] {
@@ -1515,10 +1643,14 @@ bool transfer4_enabled() {
 void launch_restrict(int64_t n_coarse, int nc, const int64_t* ptr, const int32_t* idx,
                      const double* val, const double* r_fine, const uint8_t* constrained_coarse,
                      double* b_coarse, cudaStream_t s) {
-  // restriction rows are long (a coarse node collects ~100 fine nodes): keep a
-  // thread per (row, component) for parallelism
-  transfer_kernel<<<grid_for(n_coarse * nc, 256), 256, 0, s>>>(
-      n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
+  // restriction rows are long (a coarse node collects ~100 fine nodes): a
+  // thread per (row, component), or 8 lanes per (row, component) on small levels
+  if (n_coarse < kSmallLevelNodes && small_level_kernels_enabled())
+    transfer_split_kernel<<<grid_for(n_coarse * nc * 8, 256), 256, 0, s>>>(
+        n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
+  else
+    transfer_kernel<<<grid_for(n_coarse * nc, 256), 256, 0, s>>>(
+        n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
 }
 
 void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_t* idx,
@@ -1582,7 +1714,7 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
                                                 rowslot, status);
       gj_update_kernel<<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot, status);
     }
-    gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm);
+    gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm, status);
     return 0;
   }
   // work: colk (n doubles) | rp (1 double) | perm (n int64)
@@ -1596,7 +1728,7 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
     gj_pivot_kernel<<<1, 1024, 0, s>>>(M, n, k, perm, colk, rp, status);
     gj_eliminate_kernel<<<grid, 128, 0, s>>>(M, n, k, colk, rp);
   }
-  gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm);
+  gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm, status);
   return 0;
 }
 
