@@ -127,6 +127,19 @@ def host_case_from_device(wl, prob, solver, b):
                   solver.prolongations, b)
 
 
+def apply_launches(sizes):
+    """Kernel launches of one Vanka application over patch groups of the
+    given sizes (device_kernels.cu launch_vanka_apply: consecutive groups of
+    one size share a launch, two at a time)."""
+    if os.environ.get("ALEFSI_APPLY_MERGE", "1").startswith("0"):
+        return len(sizes)
+    i, n = 0, 0
+    while i < len(sizes):
+        i += 2 if i + 1 < len(sizes) and sizes[i + 1] == sizes[i] else 1
+        n += 1
+    return n
+
+
 def kernel_bytes(case, wl):
     """Algorithmic HBM bytes of one finest-level launch of each kernel."""
     p = case.problem.levels[-1].pattern
@@ -268,8 +281,9 @@ def run_ours(args, rank, world):
             key = f"{kind}{'_finest' if finest else '_coarser'}"
             kernels[key] = {"launches": cnt, "avg_ms": ms / cnt, "share": ms / ms_prof}
     # per-application figures: a Vanka application launches one kernel per
-    # patch group (fluid, solid); kb counts the bytes of all groups
-    n_groups = len(case.patches[-1].groups)
+    # pair of consecutive same-size patch groups (fluid + solid); kb counts
+    # the bytes of all groups
+    n_groups = apply_launches(case.patches[-1].sizes())
     per_app = {"spmv": 1, "vanka_apply": n_groups}
     dom = max(("spmv", "vanka_apply"), key=lambda k: prof[(k, True)][1])
     cnt, ms = prof[(dom, True)]
