@@ -375,7 +375,21 @@ struct MgHandle {
   }
 
   // ------------------------------------------------------------ factorize
+  // buffers the captured V-cycle graph reads; a re-factorisation that keeps
+  // them (same sizes: ensure() does not reallocate) keeps the graph valid
+  std::vector<const void*> graph_buffers() const {
+    std::vector<const void*> v{coarse_inv.p};
+    for (const auto& L : lv) {
+      v.push_back(L.x.p);
+      v.push_back(L.b.p);
+      v.push_back(L.d.p);
+      for (const auto& g : L.groups) v.push_back(g->inv.p);
+    }
+    return v;
+  }
+
   int factorize() {
+    const std::vector<const void*> before = graph_buffers();
     for (int l = 1; l < n_levels; ++l) {
       Level& L = lv[l];
       if (!L.has_matrix) return fail(ALEFSI_ERR_STATE, "level matrix missing");
@@ -433,7 +447,7 @@ struct MgHandle {
       CK(L.d.ensure(L.ndof()));
     }
     factorized = true;
-    graph_valid = false;
+    if (graph_buffers() != before) graph_valid = false;
     return ALEFSI_OK;
   }
 
