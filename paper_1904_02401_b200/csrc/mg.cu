@@ -872,8 +872,8 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
   if (st != 0)
     return fail(ALEFSI_ERR_SINGULAR, "inverted element in device assembly: cell " +
                                          std::to_string(st - 1));
+  // operator values change in place: the V-cycle graph (pointers only) stays
   m->factorized = false;
-  m->graph_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }

@@ -127,8 +127,10 @@ class LinearStack:
             levels.append(linsolve.MgLevel(matrix=p.extension_blocks(l)["bc"], smoother=sm,
                                            P=self.transfers[l],
                                            constrained=lvl.ext_dirichlet.reshape(-1)))
+        # the extension operator never changes: its V-cycle is captured once
+        # and replayed as a CUDA graph
         self.ext_mg = linsolve.MgSolver(levels, self.cfg.nu_pre, self.cfg.nu_post,
-                                        use_graph=self.cfg.use_graph)
+                                        use_graph=True)
 
     def solve_extension(self, b):
         """GMRES + V-cycle on the mesh-extension system (newton.py:159-165)."""
