@@ -1033,8 +1033,6 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
   extern __shared__ __align__(16) unsigned char gj_smem[];
   double* P = reinterpret_cast<double*>(gj_smem);        // column-major: P[t * n + i]
   int* src = reinterpret_cast<int*>(P + (size_t)n * kb);  // n
-  __shared__ double sb[32];
-  __shared__ int si[32];
   __shared__ int s_pr, s_stop, s_ntouch;
   __shared__ int touched[64], srows[64];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -1046,36 +1044,33 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
   for (int i = tid; i < n; i += nt) src[i] = i;
   if (tid == 0) { s_stop = 0; s_ntouch = 0; }
   __syncthreads();
+  __shared__ double s_piv[KB], s_rk[KB];
 #pragma unroll
   for (int t = 0; t < KB; ++t) {
     if (t >= kb) break;
     const int k = k0 + t;
-    double* Pt = P + t * n;
-    double best = -1.0;
-    int bi = k;
-    for (int i = k + tid; i < n; i += nt) {
-      const double v = fabs(Pt[i]);
-      if (v > best) { best = v; bi = i; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    if ((tid & 31) == 0) { sb[tid >> 5] = best; si[tid >> 5] = bi; }
-    __syncthreads();
+    const double* Pt = P + t * n;
+    // warp 0: pivot search over column t (rows >= k), the swap bookkeeping
+    // and copies of the pivot row and old row k for everyone else
     if (tid < 32) {
-      best = tid < (nt >> 5) ? sb[tid] : -2.0;
-      bi = tid < (nt >> 5) ? si[tid] : n;
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < n; i += 32) {
+        const double v = fabs(Pt[i]);
+        if (v > best) { best = v; bi = i; }
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(0xffffffffu, best, o);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
+      const int pr = bi < n ? bi : k;
+      if (tid < kb) {
+        s_piv[tid] = P[tid * n + pr];
+        s_rk[tid] = P[tid * n + k];
+      }
       if (tid == 0) {
-        const int pr = bi < n ? bi : k;
         s_pr = pr;
         perm[k] = pr;
         if (Pt[pr] == 0.0) {
@@ -1084,23 +1079,21 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
         }
         if (s_ntouch < 64) touched[s_ntouch++] = k;
         if (pr != k && s_ntouch < 64) touched[s_ntouch++] = pr;
-        const int a = src[k];
+        const int a2 = src[k];
         src[k] = src[pr];
-        src[pr] = a;
+        src[pr] = a2;
       }
     }
     __syncthreads();
     if (s_stop) return;
     const int pr = s_pr;
-    // pivot row (old row pr) and old row k, read before anyone writes
     double piv[KB], rk[KB];
 #pragma unroll
     for (int s2 = 0; s2 < KB; ++s2) {
-      piv[s2] = s2 < kb ? P[s2 * n + pr] : 0.0;
-      rk[s2] = s2 < kb ? P[s2 * n + k] : 0.0;
+      piv[s2] = s2 < kb ? s_piv[s2] : 0.0;
+      rk[s2] = s2 < kb ? s_rk[s2] : 0.0;
     }
     const double rp = 1.0 / piv[t];
-    __syncthreads();
     // rows after the swap: row k <- old row pr (scaled), row pr <- old row k;
     // one thread per row, reading its multiplier before writing the row
     for (int i = tid; i < n; i += nt) {
