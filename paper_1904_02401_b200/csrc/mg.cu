@@ -182,9 +182,13 @@ struct MgHandle {
   double omega = 0.8;
   std::vector<Level> lv;
   DevBuf<double> coarse_inv, coarse_work;
-  DevBuf<int64_t> status;
+  DevBuf<int64_t> status, coarse_status;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // the coarse inverse is computed on a side stream, concurrently with the
+  // patch factorisations of the finer levels
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_in = nullptr, side_out = nullptr;
   bool factorized = false;
   // graph-captured V-cycle (fixed in/out buffers)
   bool use_graph = false;
@@ -219,6 +223,9 @@ struct MgHandle {
     if (cap_out) cudaEventDestroy(cap_out);
     if (pinned) cudaFreeHost(pinned);
     for (auto e : ev_pool) cudaEventDestroy(e);
+    if (side_stream) cudaStreamDestroy(side_stream);
+    if (side_in) cudaEventDestroy(side_in);
+    if (side_out) cudaEventDestroy(side_out);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -388,15 +395,67 @@ struct MgHandle {
     return v;
   }
 
+  // coarse level: dense inverse, enqueued on the side stream after the work
+  // already on the main stream (the operator's assembly)
+  int start_coarse_inverse() {
+    Level& C = lv[0];
+    if (!C.has_matrix) return fail(ALEFSI_ERR_STATE, "coarse matrix missing");
+    if (!side_stream) {
+      // high priority: the serial chain of panel steps gets an SM as soon as
+      // one frees up instead of queueing behind the patch factorisations
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&side_stream, cudaStreamNonBlocking, hi));
+      CK(cudaEventCreateWithFlags(&side_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&side_out, cudaEventDisableTiming));
+    }
+    if (!coarse_status.p) CK(coarse_status.alloc(1));
+    CK(cudaEventRecord(side_in, stream));
+    CK(cudaStreamWaitEvent(side_stream, side_in, 0));
+    const int64_t n0 = C.ndof();
+    if (!C.host_dense.empty()) {
+      CK(coarse_inv.upload(C.host_dense.data(), (size_t)n0 * n0, side_stream));
+    } else {   // device-assembled coarse operator
+      CK(coarse_inv.ensure((size_t)n0 * n0));
+      CK(cudaMemsetAsync(coarse_inv.p, 0, sizeof(double) * n0 * n0, side_stream));
+      launch_split_to_dense(C.mat(), coarse_inv.p, side_stream);
+    }
+    CK(coarse_work.ensure((size_t)dense_inverse_work(n0)));
+    if (dense_inverse(coarse_inv.p, n0, coarse_work.p, coarse_status.p, side_stream) != 0)
+      return fail(ALEFSI_ERR_ARG, "coarse level too large for the dense inverse (" +
+                                      std::to_string(n0) + " > 4096 dofs)");
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(side_out, side_stream));
+    return ALEFSI_OK;
+  }
+
+  int finish_coarse_inverse() {
+    CK(cudaStreamWaitEvent(stream, side_out, 0));
+    int64_t st = 0;
+    CK(cudaMemcpyAsync(&st, coarse_status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (st != 0) return fail(ALEFSI_ERR_SINGULAR, "singular coarse-level matrix");
+    return ALEFSI_OK;
+  }
+
   int factorize() {
     const std::vector<const void*> before = graph_buffers();
+    int rc = start_coarse_inverse();
+    if (rc) {
+      if (side_stream) cudaStreamSynchronize(side_stream);
+      return rc;
+    }
     for (int l = 1; l < n_levels; ++l) {
       Level& L = lv[l];
-      if (!L.has_matrix) return fail(ALEFSI_ERR_STATE, "level matrix missing");
-      if (!L.has_P) return fail(ALEFSI_ERR_STATE, "level prolongation missing");
-      if (L.groups.empty()) return fail(ALEFSI_ERR_STATE, "level patches missing");
+      auto bail = [&](int code, const std::string& msg) {
+        cudaStreamSynchronize(side_stream);
+        return fail(code, msg);
+      };
+      if (!L.has_matrix) return bail(ALEFSI_ERR_STATE, "level matrix missing");
+      if (!L.has_P) return bail(ALEFSI_ERR_STATE, "level prolongation missing");
+      if (L.groups.empty()) return bail(ALEFSI_ERR_STATE, "level patches missing");
       if (!L.constrained.p || !lv[l - 1].constrained.p)
-        return fail(ALEFSI_ERR_STATE, "constrained mask missing");
+        return bail(ALEFSI_ERR_STATE, "constrained mask missing");
       CK(cudaMemsetAsync(status.p, 0, sizeof(int64_t), stream));
       int64_t off = 0;
       for (auto& g : L.groups) {
@@ -414,32 +473,14 @@ struct MgHandle {
         CK(cudaMemcpyAsync(&st, status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         if (st != 0)
-          return fail(ALEFSI_ERR_SINGULAR,
+          return bail(ALEFSI_ERR_SINGULAR,
                       "singular Vanka patch block: level " + std::to_string(l) + " patch " +
                           std::to_string(off + st - 1));
         off += g->n_patches;
       }
     }
-    // coarse level: dense inverse
-    Level& C = lv[0];
-    if (!C.has_matrix) return fail(ALEFSI_ERR_STATE, "coarse matrix missing");
-    const int64_t n0 = C.ndof();
-    if (!C.host_dense.empty()) {
-      CK(coarse_inv.upload(C.host_dense.data(), (size_t)n0 * n0, stream));
-    } else {   // device-assembled coarse operator
-      CK(coarse_inv.ensure((size_t)n0 * n0));
-      CK(cudaMemsetAsync(coarse_inv.p, 0, sizeof(double) * n0 * n0, stream));
-      launch_split_to_dense(C.mat(), coarse_inv.p, stream);
-    }
-    CK(coarse_work.ensure((size_t)dense_inverse_work(n0)));
-    if (dense_inverse(coarse_inv.p, n0, coarse_work.p, status.p, stream) != 0)
-      return fail(ALEFSI_ERR_ARG, "coarse level too large for the dense inverse (" +
-                                      std::to_string(n0) + " > 4096 dofs)");
-    CK(cudaGetLastError());
-    int64_t st = 0;
-    CK(cudaMemcpyAsync(&st, status.p, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    if (st != 0) return fail(ALEFSI_ERR_SINGULAR, "singular coarse-level matrix");
+    rc = finish_coarse_inverse();
+    if (rc) return rc;
     for (int l = 0; l < n_levels; ++l) {
       Level& L = lv[l];
       CK(L.x.ensure(L.ndof()));
