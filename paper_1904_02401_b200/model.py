@@ -362,10 +362,16 @@ def _residual_tail(lvl, mats, k, theta, U, U_prev, explicit, R, device_tail=Fals
         outflow_correction(lvl, mats, U, Xc, scale=k * theta)
         R[:, 1:1 + d] += Xc
         R[:, 0] += k * (lvl.lps_csr() @ U[:, 0])
-    deficit = (U[:, 1 + d:] - U_prev[:, 1 + d:] - k * theta * U[:, 1:1 + d]
-               - k * (1.0 - theta) * U_prev[:, 1:1 + d])
-    R[lvl.relation_nodes, 1 + d:] = lvl.solid_mass_rows() @ deficit
-    R[lvl.residual_zero_mask] = 0.0
+    # the deficit is formed only on the columns the relation rows touch
+    cols, M = lvl.solid_mass_relation()
+    Uc, Upc = U[cols], U_prev[cols]
+    deficit = (Uc[:, 1 + d:] - Upc[:, 1 + d:] - k * theta * Uc[:, 1:1 + d]
+               - k * (1.0 - theta) * Upc[:, 1:1 + d])
+    R[lvl.relation_nodes, 1 + d:] = M @ deficit
+    if R.flags.c_contiguous:
+        R.reshape(-1)[lvl.residual_zero_flat()] = 0.0
+    else:
+        R[lvl.residual_zero_mask] = 0.0
     return R
 
 

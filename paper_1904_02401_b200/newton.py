@@ -199,10 +199,11 @@ def solve_reduced_linear(problem, stack, R, U, U_prev, k, theta):
     x, mom_stats = stack.solve_momentum(-R[:, :d + 1].reshape(-1))
     dpv = np.asarray(x).reshape(n, d + 1)
     rel = lvl.relation_nodes
-    deficit = (U[:, 1 + d:] - U_prev[:, 1 + d:] - k * theta * U[:, 1:1 + d]
-               - k * (1.0 - theta) * U_prev[:, 1:1 + d])
+    Ur, Upr = U[rel], U_prev[rel]      # the deficit is needed on the relation nodes only
+    deficit = (Ur[:, 1 + d:] - Upr[:, 1 + d:] - k * theta * Ur[:, 1:1 + d]
+               - k * (1.0 - theta) * Upr[:, 1:1 + d])
     du = np.zeros((n, d))
-    du[rel] = k * theta * dpv[rel, 1:] - deficit[rel]
+    du[rel] = k * theta * dpv[rel, 1:] - deficit
     blocks = problem.extension_blocks(len(problem.levels) - 1)
     g = np.zeros((n, d))
     g[lvl.interface_nodes] = du[lvl.interface_nodes]
