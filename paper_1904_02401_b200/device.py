@@ -10,6 +10,7 @@ tensors (device-resident, no copies).
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -59,16 +60,14 @@ class DeviceMgSolver:
                   C.byref(h))
         self._h = h
         self._lib = lib
-        if stream is None:
+        self._stream_bound = stream is not None
+        if stream is None and "torch" in sys.modules:
             # enqueue on torch's current stream so device tensors passed in are
-            # ordered after the work that produced them
-            try:
-                import torch
-                if torch.cuda.is_available():
-                    stream = torch.cuda.current_stream().cuda_stream
-            except ImportError:
-                pass
-        if stream is not None:
+            # ordered after the work that produced them.  Without torch loaded
+            # (host-array callers such as the time loop) the library keeps its
+            # own stream and torch is bound on first use of a device tensor.
+            self._bind_torch_stream()
+        elif stream is not None:
             _lib.call("alefsi_mg_set_stream", h, C.c_void_p(int(stream)))
         self.ndofs = []
         self._groups = {}
@@ -79,6 +78,15 @@ class DeviceMgSolver:
         _lib.call("alefsi_mg_use_graph", h, 1 if use_graph else 0)
         if factorize:
             self.factorize()
+
+    def _bind_torch_stream(self):
+        if self._stream_bound:
+            return
+        import torch
+        if torch.cuda.is_available():
+            _lib.call("alefsi_mg_set_stream", self._h,
+                      C.c_void_p(int(torch.cuda.current_stream().cuda_stream)))
+        self._stream_bound = True
 
     # -- setup ------------------------------------------------------------------
     def _set_level(self, l, lv):
@@ -176,6 +184,7 @@ class DeviceMgSolver:
         """One V-cycle (MgSolver.dot, reference linsolve.py:238-255)."""
         if _is_device(b):
             import torch
+            self._bind_torch_stream()
             z = torch.empty_like(b)
             _lib.call("alefsi_mg_apply", self._h, b, z, 0)
             return z
@@ -195,6 +204,7 @@ class DeviceMgSolver:
         conv = np.zeros(1, dtype=np.int32)
         if _is_device(b):
             import torch
+            self._bind_torch_stream()
             x = x_out if x_out is not None else torch.empty_like(b)
             host = 0
         else:
@@ -221,24 +231,29 @@ class DeviceMgSolver:
 
     # -- single kernels (parity tests, micro-benchmarks; device tensors) ------------
     def spmv(self, level, x, b=None, y=None):
+        self._bind_torch_stream()
         import torch
         y = torch.empty_like(x) if y is None else y
         _lib.call("alefsi_mg_spmv", self._h, level, x, b if b is not None else None, y)
         return y
 
     def sweep(self, level, x, b):
+        self._bind_torch_stream()
         _lib.call("alefsi_mg_vanka_sweep", self._h, level, x, b)
         return x
 
     def restrict(self, level, r_fine, out):
+        self._bind_torch_stream()
         _lib.call("alefsi_mg_restrict", self._h, level, r_fine, out)
         return out
 
     def prolong_add(self, level, x_coarse, x_fine):
+        self._bind_torch_stream()
         _lib.call("alefsi_mg_prolong_add", self._h, level, x_coarse, x_fine)
         return x_fine
 
     def coarse_solve(self, b, x):
+        self._bind_torch_stream()
         _lib.call("alefsi_mg_coarse_solve", self._h, b, x)
         return x
 
