@@ -25,7 +25,7 @@ SCALE = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "m
 
 
 def short(name):
-    return name.split("(")[0].replace("void ", "").replace("unnamed>::", "").replace(
+    return name.split("(")[0].replace("void ", "").replace("<unnamed>::", "").replace("unnamed>::", "").replace(
         "alefsi::", "")
 
 
