@@ -193,6 +193,42 @@ def test_zero_rhs_returns_zero():
     assert st.iterations == 0 and not x.any()
 
 
+def test_device_gmres_tolerance_edges_vs_oracle():
+    """Stopping rules of reference linsolve.py:55-60,107-115 on the device:
+    tol = max(rel_tol * beta, abs_tol); beta <= tol returns zero after no
+    iteration; an absolute tolerance alone stops at the oracle's iteration;
+    a failed solve raises with the same partial history."""
+    name = "3d_tiny"
+    wl = W.CONFIGS[name]
+    case = get_case(name)
+    s = solver_for(name)
+    mg = orc.MgOracle(case, wl.nu_pre, wl.nu_post, wl.omega)
+    beta = np.linalg.norm(case.b)
+    # early return: abs_tol at beta (reference: beta <= tol); the device norm
+    # is a fixed-order tree sum, equal to numpy's to the last bits only
+    x, st = s.gmres(case.b, rel_tol=0.0, abs_tol=beta * (1 + 1e-12))
+    assert st.iterations == 0 and not x.any() and len(st.residuals) == 1
+    assert abs(st.residuals[0] - beta) <= 1e-14 * beta
+    # absolute tolerance only
+    xo, so = orc.gmres(mg.A[-1], case.b, mg, rel_tol=0.0, abs_tol=1e-6 * beta, max_iter=250)
+    x, st = s.gmres(case.b, rel_tol=0.0, abs_tol=1e-6 * beta, max_iter=250)
+    assert_history(st, so.residuals, so.iterations)
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+    # the larger of the two tolerances wins
+    _, st2 = s.gmres(case.b, rel_tol=1e-6, abs_tol=1e-12 * beta, max_iter=250)
+    assert st2.iterations == so.iterations
+    # iteration limit: same partial history as the oracle's failed solve
+    with pytest.raises(orc.OracleSolverError) as eo:
+        orc.gmres(mg.A[-1], case.b, mg, rel_tol=1e-14, max_iter=4)
+    with pytest.raises(device.SolverError) as ed:
+        s.gmres(case.b, rel_tol=1e-14, max_iter=4)
+    assert_history(ed.value.stats, eo.value.stats.residuals, 4)
+    # one iteration allowed and enough
+    r1 = so.residuals[1]
+    x1, st1 = s.gmres(case.b, rel_tol=0.0, abs_tol=r1 * (1 + 1e-6), max_iter=1)
+    assert st1.iterations == 1 and st1.converged
+
+
 @pytest.mark.parametrize("name", ["2d_small", "3d_small"])
 def test_device_full_size_vs_reference_history(name):
     """BASELINE configs 0 and 2 at full size against the reference's own run."""
