@@ -487,6 +487,50 @@ __global__ void vanka_gather_kernel(int64_t ndof, int nc, const int64_t* __restr
   x[t] = __dadd_rn(base, __dmul_rn(omega, acc));
 }
 
+// NC = 4: one thread per node sums the node's 4 components together — one
+// 32-byte load of Y per (patch, local node) slot (slots are 4-aligned: every
+// patch column length and group offset is a multiple of 4) and one 32-byte
+// load / store of x.  Per component the same operations in the same order
+// as vanka_gather_kernel: bitwise-identical x.
+__global__ void vanka_gather4_kernel(int64_t n_nodes, const int64_t* __restrict__ gptr,
+                                     const int64_t* __restrict__ goff,
+                                     const double* __restrict__ w, const double* __restrict__ Y,
+                                     double* __restrict__ x, double omega, int init_zero) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= n_nodes) return;
+  const double wn = __ldg(w + n);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int64_t sb = gptr[n], se = gptr[n + 1];
+  // four slots' offsets, then their four Y loads, in flight together
+  for (int64_t s = sb; s < se; s += 4) {
+    d4 y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      y[u] = d4{0.0, 0.0, 0.0, 0.0};
+      if (s + u < se) y[u] = ld256_ro(Y + __ldg(goff + s + u));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (s + u < se) {
+        a0 = __dadd_rn(a0, __dmul_rn(wn, y[u].x));
+        a1 = __dadd_rn(a1, __dmul_rn(wn, y[u].y));
+        a2 = __dadd_rn(a2, __dmul_rn(wn, y[u].z));
+        a3 = __dadd_rn(a3, __dmul_rn(wn, y[u].w));
+      }
+    }
+  }
+  double* xn = x + 4 * n;
+  d4 base{0.0, 0.0, 0.0, 0.0};
+  if (!init_zero) base = ld256_ro(xn);
+  const double o0 = __dadd_rn(base.x, __dmul_rn(omega, a0));
+  const double o1 = __dadd_rn(base.y, __dmul_rn(omega, a1));
+  const double o2 = __dadd_rn(base.z, __dmul_rn(omega, a2));
+  const double o3 = __dadd_rn(base.w, __dmul_rn(omega, a3));
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(xn), "d"(o0), "d"(o1), "d"(o2),
+               "d"(o3)
+               : "memory");
+}
+
 template <int I>
 struct IntC {
   static constexpr int value = I;
@@ -1606,11 +1650,29 @@ int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const 
   return launches;
 }
 
+// ALEFSI_GATHER4=0 keeps the thread-per-dof gather for NC = 4 (A/B only)
+bool gather4_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_GATHER4");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int64_t* goff,
                          const double* weight, const double* Y, double* x, double omega,
                          int init_zero, cudaStream_t s) {
   const int64_t ndof = n_nodes * nc;
   if (ndof == 0) return;
+  // large levels only: on small, latency-bound levels a thread per dof
+  // (4x the threads) is faster
+  if (nc == 4 && n_nodes >= kSmallLevelNodes && gather4_enabled() &&
+      reinterpret_cast<uintptr_t>(Y) % 32 == 0 &&
+      reinterpret_cast<uintptr_t>(x) % 32 == 0) {
+    vanka_gather4_kernel<<<grid_for(n_nodes, 256), 256, 0, s>>>(n_nodes, gptr, goff, weight, Y,
+                                                                 x, omega, init_zero);
+    return;
+  }
   vanka_gather_kernel<<<grid_for(ndof, 256), 256, 0, s>>>(ndof, nc, gptr, goff, weight, Y, x,
                                                            omega, init_zero);
 }
