@@ -547,13 +547,20 @@ struct IntC {
 // next pivot with a warp-local argmax right after its own share of the
 // step-k elimination, overlapped with the other warps' eliminations: two
 // block barriers per pivot step, no single-warp phase on the critical path.
-template <int NP, int NC, int W, int NPAT>
-__global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
+// TAIL > 0 (NPAT = 1): the last register row holds only TAIL real rows
+// (108 = 3 x 32 + 12); those rows live in shared memory instead, which
+// brings the kernel under the register budget of two CTAs per SM, so two
+// patches' pivot chains overlap.  Same operations: bitwise-equal inverses.
+template <int NP, int NC, int W, int NPAT, int TAIL = 0>
+__global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_kernel(
     DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, RT = (NP + 31) / 32, CT = (NP + W - 1) / W, NT = 32 * W;
   static_assert(RT <= 4, "pivot-row scaling covers up to 4 register rows");
   constexpr int NR = 32 * RT, NCOL = W * CT;               // padded row / column counts
+  constexpr int RTR = TAIL > 0 ? RT - 1 : RT;               // register rows
+  static_assert(TAIL == 0 || (NPAT == 1 && TAIL == NP - 32 * RTR), "tail rows");
+  __shared__ double Mt[TAIL > 0 ? TAIL : 1][NCOL + 1];     // +1: conflict-free rows
   __shared__ int32_t slotB[NPAT][NPN * NPN], slotP[NPAT][NPN * NPN];
   __shared__ double colk[NPAT][2][NR], prow[NPAT][NCOL], pivval[NPAT];
   __shared__ int used[NPAT][NP], piv_of_step[NPAT][NP], step_of_row[NPAT][NP];
@@ -596,7 +603,7 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
   }
   for (int i = tid; i < NPAT * NP; i += NT) used[i / NP][i % NP] = 0;
   __syncthreads();
-  double M[NPAT][RT][CT];
+  double M[NPAT][RTR][CT];
 #pragma unroll
   for (int q = 0; q < NPAT; ++q)
 #pragma unroll
@@ -612,7 +619,9 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
           if (slotB[q][t] >= 0) v = A.data[(int64_t)slotB[q][t] * (NC * NC) + ci * NC + cj];
           else if (ci == 0 && cj == 0 && slotP[q][t] >= 0) v = A.pp_data[slotP[q][t]];
         }
-        M[q][i][j] = v;
+        if constexpr (TAIL == 0) M[q][i][j] = v;
+        else if (i < RTR) M[q][i < RTR ? i : 0][j] = v;
+        else if (ty < TAIL) Mt[ty][c] = v;
       }
   // owner warp of column k: publish it and choose its pivot (largest |.| of
   // the unused rows, lowest index on ties)
@@ -627,12 +636,18 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
       for (int i = 0; i < RT; ++i) {
         const int r = ty + 32 * i;
         double v = 0.0;
+        if (TAIL == 0 || i < RTR) {
 #pragma unroll
-        for (int j = 0; j < CT; ++j) {
-          if (j == jk) v = M[q][i][j];
-          // column k restarts from 0: the elimination's fma then yields
-          // -f * (1/pivot) there, with no per-element select
-          M[q][i][j] = (j == jk) ? 0.0 : M[q][i][j];
+          for (int j = 0; j < CT; ++j) {
+            const int ir = TAIL == 0 ? i : (i < RTR ? i : 0);
+            if (j == jk) v = M[q][ir][j];
+            // column k restarts from 0: the elimination's fma then yields
+            // -f * (1/pivot) there, with no per-element select
+            M[q][ir][j] = (j == jk) ? 0.0 : M[q][ir][j];
+          }
+        } else if (ty < TAIL) {
+          v = Mt[ty][k];
+          Mt[ty][k] = 0.0;
         }
         if (r < NP) {
           colk[q][k & 1][r] = v;
@@ -679,9 +694,15 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
 #pragma unroll
           for (int j = 0; j < CT; ++j) {
             const int c = w + W * j;
-            const double v = (c == k) ? rp[q] : M[q][i][j] * rp[q];
-            M[q][i][j] = v;
-            if (c < NP) prow[q][c] = v;
+            if constexpr (i < RTR) {
+              const double v = (c == k) ? rp[q] : M[q][i][j] * rp[q];
+              M[q][i][j] = v;
+              if (c < NP) prow[q][c] = v;
+            } else {
+              const double v = (c == k) ? rp[q] : Mt[ty][c] * rp[q];
+              Mt[ty][c] = v;
+              if (c < NP) prow[q][c] = v;
+            }
           }
         };
         switch (pr[q] >> 5) {
@@ -705,10 +726,17 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
 #pragma unroll
       for (int j = 0; j < CT; ++j) pv[j] = prow[q][w + W * j];
 #pragma unroll
-      for (int i = 0; i < RT; ++i) {
+      for (int i = 0; i < RTR; ++i) {
         const double nf = -ck[ty + 32 * i];
 #pragma unroll
         for (int j = 0; j < CT; ++j) M[q][i][j] = fma(nf, pv[j], M[q][i][j]);
+      }
+      if constexpr (TAIL > 0) {
+        if (ty < TAIL) {
+          const double nf = -ck[ty + 32 * RTR];
+#pragma unroll
+          for (int j = 0; j < CT; ++j) Mt[ty][w + W * j] = fma(nf, pv[j], Mt[ty][w + W * j]);
+        }
       }
     }
     if (k + 1 < NP) owner_step(k + 1);
@@ -724,7 +752,8 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
       for (int j = 0; j < CT; ++j) {
         const int r = ty + 32 * i, c = w + W * j;
         if (r < NP && c < NP)
-          out[(int64_t)piv_of_step[q][c] * ld + step_of_row[q][r]] = M[q][i][j];
+          out[(int64_t)piv_of_step[q][c] * ld + step_of_row[q][r]] =
+              (TAIL == 0 || i < RTR) ? M[q][TAIL == 0 ? i : (i < RTR ? i : 0)][j] : Mt[ty][c];
       }
     if (ld > NP)
       for (int col = tid; col < NP; col += NT)
@@ -1591,12 +1620,24 @@ void factorize_big(const DevMatrix& A, const DevPatchGroup& g, int64_t* status, 
   cudaFree(perm);
 }
 
-template <int NP, int NC, int W, int NPAT>
+template <int NP, int NC, int W, int NPAT, int TAIL = 0>
 void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                            cudaStream_t s) {
   const unsigned grid = (unsigned)((g.n_patches + NPAT - 1) / NPAT);
-  vanka_factorize_cw_kernel<NP, NC, W, NPAT><<<grid, 32 * W, 0, s>>>(A, g.n_patches, g.nodes,
-                                                                    g.inv, g.ld, status);
+  vanka_factorize_cw_kernel<NP, NC, W, NPAT, TAIL><<<grid, 32 * W, 0, s>>>(
+      A, g.n_patches, g.nodes, g.inv, g.ld, status);
+}
+
+constexpr int64_t kTailMinPatches = 32768;
+
+// ALEFSI_FACT_TAIL=0 keeps all rows of the 108 x 108 patches in registers
+// (one CTA per SM; A/B only)
+bool fact_tail_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_FACT_TAIL");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
 }
 
 }  // namespace
@@ -1619,7 +1660,14 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
   if (g.n_patches == 0) return;
   if (A.nc == 3 && g.np == 27) factorize_cw_dispatch<27, 3, 3, 2>(A, g, status, s);
   else if (A.nc == 3 && g.np == 75) factorize_cw_dispatch<75, 3, 8, 2>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108) factorize_cw_dispatch<108, 4, 12, 1>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108) {
+    // two CTAs per SM fill every SM, which leaves no room for the coarse
+    // inverse's 218 KB panel CTAs on the side stream: only for groups large
+    // enough that the patch work dominates (config 3: 136 -> 104 ms)
+    if (fact_tail_enabled() && g.n_patches >= kTailMinPatches)
+      factorize_cw_dispatch<108, 4, 12, 1, 12>(A, g, status, s);
+    else factorize_cw_dispatch<108, 4, 12, 1>(A, g, status, s);
+  }
   else if (A.nc == 2 && g.np == 18) factorize_cw_dispatch<18, 2, 2, 2>(A, g, status, s);
   else if (A.nc == 3 && g.np == 81) factorize_cw_dispatch<81, 3, 9, 2>(A, g, status, s);
   else if (A.nc == 4 && g.np == 500) factorize_big(A, g, status, s);
