@@ -1630,8 +1630,8 @@ void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* 
 
 constexpr int64_t kTailMinPatches = 32768;
 
-// ALEFSI_FACT_TAIL=0 keeps all rows of the 108 x 108 patches in registers
-// (one CTA per SM; A/B only)
+// ALEFSI_FACT_TAIL=0 (A/B only): the one-CTA-per-SM forms — all rows of the
+// 108 x 108 patches in registers, two 75 x 75 patches per CTA
 bool fact_tail_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("ALEFSI_FACT_TAIL");
@@ -1659,7 +1659,12 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
                             cudaStream_t s) {
   if (g.n_patches == 0) return;
   if (A.nc == 3 && g.np == 27) factorize_cw_dispatch<27, 3, 3, 2>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 75) factorize_cw_dispatch<75, 3, 8, 2>(A, g, status, s);
+  else if (A.nc == 3 && g.np == 75) {
+    // one patch per CTA (118 registers, two CTAs per SM) instead of two per
+    // CTA (178 registers, one CTA): config 1 80 -> 70 ms, bitwise equal
+    if (fact_tail_enabled()) factorize_cw_dispatch<75, 3, 8, 1>(A, g, status, s);
+    else factorize_cw_dispatch<75, 3, 8, 2>(A, g, status, s);
+  }
   else if (A.nc == 4 && g.np == 108) {
     // two CTAs per SM fill every SM, which leaves no room for the coarse
     // inverse's 218 KB panel CTAs on the side stream: only for groups large
