@@ -1108,7 +1108,21 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
   int* src = reinterpret_cast<int*>(P + (size_t)n * kb);  // n
   __shared__ int s_pr, s_stop, s_ntouch;
   __shared__ int touched[64], srows[64];
-  const int tid = threadIdx.x, nt = blockDim.x;
+  // per-warp pivot candidates (|value|, row) of the next pivot column: each
+  // step's row update also scans the column the next step pivots on, so the
+  // pivot search is spread over all warps instead of a 32-lane scan of n rows
+  // between two barriers (same choice: largest |value|, lowest row on ties)
+  __shared__ double cand_v[32];
+  __shared__ int cand_i[32];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  auto warp_argmax = [&](double& best, int& bi) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+  };
   if (*status != 0) return;   // an earlier panel hit a zero pivot
   for (int e = tid; e < n * kb; e += nt) {
     const int i = e / kb, t = e - i * kb;
@@ -1117,27 +1131,29 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
   for (int i = tid; i < n; i += nt) src[i] = i;
   if (tid == 0) { s_stop = 0; s_ntouch = 0; }
   __syncthreads();
+  {
+    double best = -1.0;
+    int bi = n;
+    for (int i = k0 + tid; i < n; i += nt) {
+      const double v = fabs(P[i]);
+      if (v > best) { best = v; bi = i; }
+    }
+    warp_argmax(best, bi);
+    if (lane == 0) { cand_v[wid] = best; cand_i[wid] = bi; }
+  }
+  __syncthreads();
   __shared__ double s_piv[KB], s_rk[KB];
 #pragma unroll
   for (int t = 0; t < KB; ++t) {
     if (t >= kb) break;
     const int k = k0 + t;
     const double* Pt = P + t * n;
-    // warp 0: pivot search over column t (rows >= k), the swap bookkeeping
-    // and copies of the pivot row and old row k for everyone else
+    // warp 0: pivot of column t (rows >= k) from the warps' candidates, the
+    // swap bookkeeping and copies of the pivot row and old row k
     if (tid < 32) {
-      double best = -1.0;
-      int bi = k;
-      for (int i = k + tid; i < n; i += 32) {
-        const double v = fabs(Pt[i]);
-        if (v > best) { best = v; bi = i; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
+      double best = lane < nt / 32 ? cand_v[lane] : -1.0;
+      int bi = lane < nt / 32 ? cand_i[lane] : n;
+      warp_argmax(best, bi);
       const int pr = bi < n ? bi : k;
       if (tid < kb) {
         s_piv[tid] = P[tid * n + pr];
@@ -1169,6 +1185,8 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
     const double rp = 1.0 / piv[t];
     // rows after the swap: row k <- old row pr (scaled), row pr <- old row k;
     // one thread per row, reading its multiplier before writing the row
+    double nbest = -1.0;
+    int nbi = n;
     for (int i = tid; i < n; i += nt) {
       if (i == k) {
 #pragma unroll
@@ -1182,7 +1200,19 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
       const double f = row[t];
 #pragma unroll
       for (int s2 = 0; s2 < KB; ++s2)
-        if (s2 < kb) P[s2 * n + i] = (s2 == t) ? -f * rp : row[s2] - f * (piv[s2] * rp);
+        if (s2 < kb) {
+          const double v = (s2 == t) ? -f * rp : row[s2] - f * (piv[s2] * rp);
+          P[s2 * n + i] = v;
+          // next pivot column: rows >= k + 1, ascending within the thread
+          if (s2 == t + 1 && i > k) {
+            const double a = fabs(v);
+            if (a > nbest) { nbest = a; nbi = i; }
+          }
+        }
+    }
+    if (t + 1 < kb) {
+      warp_argmax(nbest, nbi);
+      if (lane == 0) { cand_v[wid] = nbest; cand_i[wid] = nbi; }
     }
     __syncthreads();
   }
@@ -1797,13 +1827,14 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
     int* rowslot = src + n;
     double* slab = work + 2 * n;
     const size_t smem = (size_t)n * nb * 8 + (size_t)n * 4;
+    // dynamic + static shared memory must stay within the 227 KB per CTA
     static bool attr = [] {
       cudaFuncSetAttribute(gj_panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           226 * 1024);
+                           225 * 1024);
       cudaFuncSetAttribute(gj_panel_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           226 * 1024);
+                           225 * 1024);
       cudaFuncSetAttribute(gj_panel_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           226 * 1024);
+                           225 * 1024);
       return true;
     }();
     (void)attr;
