@@ -7,6 +7,7 @@
 // evict-first hints for data read once per sweep (operator blocks, patch
 // inverses), read-only-path loads for vectors reused from L2, and fixed-order
 // reductions so that every result is bitwise reproducible run to run.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -1249,6 +1250,216 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
   }
 }
 
+// The same panel factorisation spread over a thread-block cluster of C CTAs
+// (distributed shared memory): CTA c holds rows [c*R, (c+1)*R) of the
+// n x kb panel, so the panel load, the row updates and the per-step pivot
+// scans run on C SMs instead of one.  Per pivot step: every CTA publishes its
+// best candidate, all CTAs pick the same pivot from the C candidates (largest
+// |value|, lowest row on ties: the single-CTA choice), the owners of the
+// pivot row and of row k publish their old values, and every CTA updates its
+// rows with the single-CTA kernel's arithmetic — two cluster barriers per
+// step, bitwise-equal panels.  Rank 0 keeps the permutation bookkeeping and
+// the snapshot rows exactly as gj_panel_kernel does.
+template <int KB>
+__global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n, int k0, int kb,
+                                                               int R, int64_t* perm,
+                                                               int* src_out, double* slab,
+                                                               int* rowslot, int64_t* status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks(), cr = (int)cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char gjc_smem[];
+  double* P = reinterpret_cast<double*>(gjc_smem);        // column-major: P[t * R + local row]
+  int* src = reinterpret_cast<int*>(P + (size_t)R * kb);  // n (rank 0)
+  __shared__ double cand_v[8], cta_v, pivrow[KB], rkrow[KB], lp[KB], lk[KB];
+  __shared__ int cand_i[8], cta_i, s_pr, s_ntouch;
+  __shared__ int touched[64], srows[64];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int r0 = cr * R, r1 = min(n, r0 + R), nr = max(0, r1 - r0);
+  auto warp_argmax = [&](double& best, int& bi) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+  };
+  // per-warp candidates -> this CTA's candidate (warp 0), after a CTA barrier
+  auto cta_argmax = [&]() {
+    __syncthreads();
+    if (tid < 32) {
+      double best = lane < nt / 32 ? cand_v[lane] : -1.0;
+      int bi = lane < nt / 32 ? cand_i[lane] : n;
+      warp_argmax(best, bi);
+      if (lane == 0) { cta_v = best; cta_i = bi; }
+    }
+  };
+  if (*status != 0) return;   // an earlier panel hit a zero pivot (every CTA sees it)
+  constexpr int LB = 8;         // global loads in flight per thread in the copies
+  for (int e0 = tid; e0 < nr * kb; e0 += LB * nt) {
+    double v[LB];
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int e = e0 + u * nt;
+      if (e < nr * kb) {
+        const int il = e / kb, t = e - il * kb;
+        v[u] = M[(int64_t)(r0 + il) * n + k0 + t];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int e = e0 + u * nt;
+      if (e < nr * kb) {
+        const int il = e / kb, t = e - il * kb;
+        P[t * R + il] = v[u];
+      }
+    }
+  }
+  if (cr == 0) {
+    for (int i = tid; i < n; i += nt) src[i] = i;
+    if (tid == 0) s_ntouch = 0;
+  }
+  __syncthreads();
+  {
+    double best = -1.0;
+    int bi = n;
+    for (int il = tid; il < nr; il += nt)
+      if (r0 + il >= k0) {
+        const double v = fabs(P[il]);
+        if (v > best) { best = v; bi = r0 + il; }
+      }
+    warp_argmax(best, bi);
+    if (lane == 0) { cand_v[wid] = best; cand_i[wid] = bi; }
+  }
+  cta_argmax();
+  cluster.sync();
+#pragma unroll
+  for (int t = 0; t < KB; ++t) {
+    if (t >= kb) break;
+    const int k = k0 + t;
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = n;
+      if (lane < C) {
+        best = *cluster.map_shared_rank(&cta_v, lane);
+        bi = *cluster.map_shared_rank(&cta_i, lane);
+      }
+      warp_argmax(best, bi);
+      if (lane == 0) s_pr = bi < n ? bi : k;
+    }
+    __syncthreads();
+    const int pr = s_pr;
+    if (tid < kb) {
+      if (pr >= r0 && pr < r1) pivrow[tid] = P[tid * R + pr - r0];
+      if (k >= r0 && k < r1) rkrow[tid] = P[tid * R + k - r0];
+    }
+    cluster.sync();   // (A) old pivot row and old row k published
+    if (tid < kb) {
+      lp[tid] = *cluster.map_shared_rank(&pivrow[tid], pr / R);
+      lk[tid] = *cluster.map_shared_rank(&rkrow[tid], k / R);
+    }
+    __syncthreads();
+    double piv[KB], rk[KB];
+#pragma unroll
+    for (int s2 = 0; s2 < KB; ++s2) {
+      piv[s2] = s2 < kb ? lp[s2] : 0.0;
+      rk[s2] = s2 < kb ? lk[s2] : 0.0;
+    }
+    if (piv[t] == 0.0) {   // same value in every CTA: all leave together
+      if (cr == 0 && tid == 0) {
+        perm[k] = pr;
+        if (*status == 0) *status = k + 1;
+      }
+      return;
+    }
+    if (cr == 0 && tid == 0) {
+      perm[k] = pr;
+      if (s_ntouch < 64) touched[s_ntouch++] = k;
+      if (pr != k && s_ntouch < 64) touched[s_ntouch++] = pr;
+      const int a2 = src[k];
+      src[k] = src[pr];
+      src[pr] = a2;
+    }
+    const double rp = 1.0 / piv[t];
+    double nbest = -1.0;
+    int nbi = n;
+    for (int il = tid; il < nr; il += nt) {
+      const int i = r0 + il;
+      if (i == k) {
+#pragma unroll
+        for (int s2 = 0; s2 < KB; ++s2)
+          if (s2 < kb) P[s2 * R + il] = (s2 == t) ? rp : piv[s2] * rp;
+        continue;
+      }
+      double row[KB];
+#pragma unroll
+      for (int s2 = 0; s2 < KB; ++s2) row[s2] = s2 < kb ? (i == pr ? rk[s2] : P[s2 * R + il]) : 0.0;
+      const double f = row[t];
+#pragma unroll
+      for (int s2 = 0; s2 < KB; ++s2)
+        if (s2 < kb) {
+          const double v = (s2 == t) ? -f * rp : row[s2] - f * (piv[s2] * rp);
+          P[s2 * R + il] = v;
+          if (s2 == t + 1 && i > k) {
+            const double a = fabs(v);
+            if (a > nbest) { nbest = a; nbi = i; }
+          }
+        }
+    }
+    warp_argmax(nbest, nbi);
+    if (lane == 0) { cand_v[wid] = nbest; cand_i[wid] = nbi; }
+    cta_argmax();
+    cluster.sync();   // (B) next candidates published; pivot rows read by all
+  }
+  for (int e = tid; e < nr * kb; e += nt) {
+    const int il = e / kb, t = e - il * kb;
+    M[(int64_t)(r0 + il) * n + k0 + t] = P[t * R + il];
+  }
+  cluster.sync();     // panel columns of M complete before the row snapshots
+  if (cr == 0) {
+    for (int i = tid; i < n; i += nt) {
+      src_out[i] = src[i];
+      rowslot[i] = -1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int q = 0;
+      for (int a = 0; a < s_ntouch; ++a) {
+        const int r = src[touched[a]];
+        bool seen = false;
+        for (int c = 0; c < q; ++c) seen = seen || srows[c] == r;
+        if (!seen) {
+          rowslot[r] = q;
+          srows[q++] = r;
+        }
+      }
+      s_ntouch = q;
+    }
+  }
+  cluster.sync();     // snapshot row list ready in rank 0
+  // every CTA copies its share of the snapshot rows, eight loads in flight
+  const int nsr = *cluster.map_shared_rank(&s_ntouch, 0);
+  if (tid < nsr) touched[tid] = *cluster.map_shared_rank(&srows[tid], 0);
+  __syncthreads();
+  const int64_t ncopy = (int64_t)nsr * n;
+  const int64_t gstride = (int64_t)C * nt;
+  for (int64_t e0 = (int64_t)cr * nt + tid; e0 < ncopy; e0 += LB * gstride) {
+    double v[LB];
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int64_t e = e0 + u * gstride;
+      if (e < ncopy) {
+        const int q = (int)(e / n), j = (int)(e - (int64_t)q * n);
+        v[u] = M[(int64_t)touched[q] * n + j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u)
+      if (e0 + u * gstride < ncopy) slab[e0 + u * gstride] = v[u];
+  }
+  cluster.sync();     // rank 0's shared memory stays valid until every CTA has read it
+}
+
 // rank-kb application of a factorised panel to the other columns (see
 // gj_panel_kernel).  CTA tile: 32 rows x 128 columns, thread = one column x
 // 16 rows (coalesced row segments); the tile's permutation sources, panel
@@ -1818,8 +2029,20 @@ bool gj_blocked_enabled() {
   return on;
 }
 
+// ALEFSI_GJ_CLUSTER=0 keeps the single-CTA panel kernel (A/B only)
+bool gj_cluster_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ALEFSI_GJ_CLUSTER");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+constexpr int kGjCluster = 8;   // CTAs per panel (portable cluster size)
+
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s) {
-  const int nb = gj_blocked_enabled() ? gj_panel_width(n) : 0;
+  // cluster panels: the n x 16 panel spread over 8 SMs fits for every n <= kGjMaxN
+  const bool clus = gj_blocked_enabled() && gj_cluster_enabled() && n >= 64;
+  const int nb = clus ? 16 : gj_blocked_enabled() ? gj_panel_width(n) : 0;
   if (nb > 0 && n <= kGjMaxN) {
     // work: perm (n int64) | src (n int) | rowslot (n int) | slab (2 nb x n)
     int64_t* perm = reinterpret_cast<int64_t*>(work);
@@ -1840,9 +2063,32 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
     (void)attr;
     cudaMemsetAsync(status, 0, sizeof(int64_t), s);
     const dim3 ug((unsigned)grid_for(n, 128), (unsigned)grid_for(n, 32));
+    const int R = (int)((n + kGjCluster - 1) / kGjCluster);
+    const size_t csmem = (size_t)R * 16 * 8 + (size_t)n * 4;
+    static bool cattr = [] {
+      cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      return true;
+    }();
+    (void)cattr;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute cat[1];
+    cat[0].id = cudaLaunchAttributeClusterDimension;
+    cat[0].val.clusterDim.x = kGjCluster;
+    cat[0].val.clusterDim.y = 1;
+    cat[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(kGjCluster);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = csmem;
+    cfg.stream = s;
+    cfg.attrs = cat;
+    cfg.numAttrs = 1;
     for (int64_t k0 = 0; k0 < n; k0 += nb) {
       const int kb = (int)std::min<int64_t>(nb, n - k0);
-      if (nb == 16)
+      if (clus)
+        cudaLaunchKernelEx(&cfg, gj_panel_cluster_kernel<16>, M, (int)n, (int)k0, kb, R, perm, src,
+                           slab, rowslot, status);
+      else if (nb == 16)
         gj_panel_kernel<16><<<1, 512, smem, s>>>(M, (int)n, (int)k0, kb, perm, src, slab,
                                                  rowslot, status);
       else if (nb == 8)
