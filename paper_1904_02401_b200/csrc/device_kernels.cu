@@ -1493,13 +1493,19 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0
   __syncthreads();
   const int jj = tid & 127, j = j0 + jj;
   if (j >= n || (j >= k0 && j < k0 + kb)) return;
+  // this thread's column of the pivot-row segments, reused for its 16 rows
+  double sk[16];
+#pragma unroll
+  for (int s2 = 0; s2 < 16; ++s2) sk[s2] = s2 < kb ? sK[s2][jj] : 0.0;
 #pragma unroll 4
   for (int r = tid >> 7; r < 32; r += 2) {
     const int i = i0 + r;
     if (i >= n) break;
     const int rs = rsrc[r];
     double acc = rs == -2 ? 0.0 : (rs == -1 ? M[(int64_t)i * n + j] : slab[(int64_t)rs * n + j]);
-    for (int s2 = 0; s2 < kb; ++s2) acc = fma(cf[r][s2], sK[s2][jj], acc);
+#pragma unroll
+    for (int s2 = 0; s2 < 16; ++s2)
+      if (s2 < kb) acc = fma(cf[r][s2], sk[s2], acc);
     M[(int64_t)i * n + j] = acc;
   }
 }
