@@ -1875,7 +1875,7 @@ void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* 
       A, g.n_patches, g.nodes, g.inv, g.ld, status);
 }
 
-constexpr int64_t kTailMinPatches = 32768;
+constexpr int64_t kTailMinPatches = 8192;
 
 // ALEFSI_FACT_TAIL=0 (A/B only): the one-CTA-per-SM forms — all rows of the
 // 108 x 108 patches in registers, two 75 x 75 patches per CTA
@@ -1913,9 +1913,8 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
     else factorize_cw_dispatch<75, 3, 8, 2>(A, g, status, s);
   }
   else if (A.nc == 4 && g.np == 108) {
-    // two CTAs per SM fill every SM, which leaves no room for the coarse
-    // inverse's 218 KB panel CTAs on the side stream: only for groups large
-    // enough that the patch work dominates (config 3: 136 -> 104 ms)
+    // two CTAs per SM; groups of >= 8192 patches (config 3: 134 -> 102 ms;
+    // config 2, whose factorisation time is the coarse inverse's, unchanged)
     if (fact_tail_enabled() && g.n_patches >= kTailMinPatches)
       factorize_cw_dispatch<108, 4, 12, 1, 12>(A, g, status, s);
     else factorize_cw_dispatch<108, 4, 12, 1>(A, g, status, s);
