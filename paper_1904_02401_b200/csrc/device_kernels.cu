@@ -1370,6 +1370,8 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
         perm[k] = pr;
         if (*status == 0) *status = k + 1;
       }
+      // no CTA may exit while another still reads its shared memory
+      cluster.sync();
       return;
     }
     if (cr == 0 && tid == 0) {
@@ -2034,18 +2036,41 @@ bool gj_blocked_enabled() {
   return on;
 }
 
-// ALEFSI_GJ_CLUSTER=0 keeps the single-CTA panel kernel (A/B only)
-bool gj_cluster_enabled() {
-  static const bool on = [] {
+// ALEFSI_GJ_CLUSTER (A/B only): CTAs per cluster panel; 0 = single-CTA
+// panel kernel.  Default: 16 (non-portable size, 2d config 0 39.5 -> 37 ms vs
+// 8) where the device can co-schedule it, else 8
+int gj_cluster_size() {
+  static const int c = [] {
     const char* e = std::getenv("ALEFSI_GJ_CLUSTER");
-    return e == nullptr || e[0] != '0';
+    if (e != nullptr) return std::atoi(e);
+    cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute cat[1];
+    cat[0].id = cudaLaunchAttributeClusterDimension;
+    cat[0].val.clusterDim.x = 16;
+    cat[0].val.clusterDim.y = 1;
+    cat[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(256);
+    // the largest panel share: kGjMaxN rows over 16 CTAs
+    cfg.dynamicSmemBytes = (size_t)(kGjMaxN / 16) * 16 * 8 + (size_t)kGjMaxN * 4;
+    cfg.attrs = cat;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, gj_panel_cluster_kernel<16>,
+                                                   &cfg) == cudaSuccess && nclusters > 0;
+    cudaGetLastError();   // a refused query leaves no sticky error
+    return ok ? 16 : 8;
   }();
-  return on;
+  return c;
 }
-constexpr int kGjCluster = 8;   // CTAs per panel (portable cluster size)
+bool gj_cluster_enabled() { return gj_cluster_size() > 0; }
 
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s) {
-  // cluster panels: the n x 16 panel spread over 8 SMs fits for every n <= kGjMaxN
+  // cluster panels: the n x 16 panel spread over 8-16 SMs fits for every n <= kGjMaxN
   const bool clus = gj_blocked_enabled() && gj_cluster_enabled() && n >= 64;
   const int nb = clus ? 16 : gj_blocked_enabled() ? gj_panel_width(n) : 0;
   if (nb > 0 && n <= kGjMaxN) {
@@ -2068,11 +2093,14 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
     (void)attr;
     cudaMemsetAsync(status, 0, sizeof(int64_t), s);
     const dim3 ug((unsigned)grid_for(n, 128), (unsigned)grid_for(n, 32));
+    const int kGjCluster = gj_cluster_size() > 0 ? gj_cluster_size() : 8;   // CTAs per panel
     const int R = (int)((n + kGjCluster - 1) / kGjCluster);
     const size_t csmem = (size_t)R * 16 * 8 + (size_t)n * 4;
     static bool cattr = [] {
       cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+      cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       return true;
     }();
     (void)cattr;
