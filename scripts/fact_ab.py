@@ -1,4 +1,5 @@
-"""Patch-factorisation A/B on the GPU box (ALEFSI_FACT_ONEBAR=0|1).
+"""Vanka + coarse factorisation A/B on the GPU box (ALEFSI_FACT_TAIL,
+ALEFSI_GJ_CLUSTER, ALEFSI_GJ_BLOCKED switches).
 
     python scripts/fact_ab.py [workload ...]
 
@@ -34,7 +35,8 @@ def main():
         sol, st = mg.gmres(b, rel_tol=wl.rel_tol, max_iter=getattr(wl, "max_iter", 250))
         h = hashlib.sha256((sol.cpu().numpy() if hasattr(sol, "cpu") else np.asarray(sol)).tobytes()).hexdigest()[:16]
         hh = hashlib.sha256(np.asarray(st.residuals).tobytes()).hexdigest()[:16]
-        print(json.dumps({"workload": name, "onebar": os.environ.get("ALEFSI_FACT_ONEBAR", "1"),
+        env = {k: v for k, v in os.environ.items() if k.startswith("ALEFSI_")}
+        print(json.dumps({"workload": name, "env": env,
                           "factorize_s": ts, "its": st.iterations, "hash_x": h,
                           "hash_history": hh}), flush=True)
         del mg, prob
