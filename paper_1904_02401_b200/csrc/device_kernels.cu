@@ -1257,8 +1257,10 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
 // best candidate, all CTAs pick the same pivot from the C candidates (largest
 // |value|, lowest row on ties: the single-CTA choice), the owners of the
 // pivot row and of row k publish their old values, and every CTA updates its
-// rows with the single-CTA kernel's arithmetic — two cluster barriers per
-// step, bitwise-equal panels.  Rank 0 keeps the permutation bookkeeping and
+// rows with the single-CTA kernel's arithmetic.  Each CTA's candidate
+// carries its row and the owner of the next row k publishes it, both in the
+// CTA's own shared memory, double-buffered by step parity: one cluster
+// barrier per step, remote loads only; bitwise-equal panels.  Rank 0 keeps the permutation bookkeeping and
 // the snapshot rows exactly as gj_panel_kernel does.
 template <int KB>
 __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n, int k0, int kb,
@@ -1271,8 +1273,12 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
   extern __shared__ __align__(16) unsigned char gjc_smem[];
   double* P = reinterpret_cast<double*>(gjc_smem);        // column-major: P[t * R + local row]
   int* src = reinterpret_cast<int*>(P + (size_t)R * kb);  // n (rank 0)
-  __shared__ double cand_v[8], cta_v, pivrow[KB], rkrow[KB], lp[KB], lk[KB];
-  __shared__ int cand_i[8], cta_i, s_pr, s_ntouch;
+  // per-CTA publication for the next step, double-buffered by step parity
+  // (read remotely by every CTA after one cluster barrier): the CTA's best
+  // candidate of the step's pivot column with that row's old values, and old
+  // row k from its owner
+  __shared__ double cand_v[8], cta_v[2], candrow[2][KB], rkrow[2][KB], lp[KB], lk[KB];
+  __shared__ int cand_i[8], cta_i[2], s_pr, s_ntouch;
   __shared__ int touched[64], srows[64];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int r0 = cr * R, r1 = min(n, r0 + R), nr = max(0, r1 - r0);
@@ -1284,14 +1290,20 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
   };
-  // per-warp candidates -> this CTA's candidate (warp 0), after a CTA barrier
-  auto cta_argmax = [&]() {
+  // per-warp candidates -> this CTA's candidate for step t with its row
+  // (warp 0), old row k0 + t from its owner (warp 1), after a CTA barrier
+  auto cta_publish = [&](int t) {
     __syncthreads();
+    const int bf = t & 1;
     if (tid < 32) {
       double best = lane < nt / 32 ? cand_v[lane] : -1.0;
       int bi = lane < nt / 32 ? cand_i[lane] : n;
       warp_argmax(best, bi);
-      if (lane == 0) { cta_v = best; cta_i = bi; }
+      if (lane == 0) { cta_v[bf] = best; cta_i[bf] = bi; }
+      if (lane < kb) candrow[bf][lane] = bi < n ? P[lane * R + bi - r0] : 0.0;
+    } else if (tid < 64) {
+      const int k = k0 + t;
+      if (k >= r0 && k < r1 && lane < kb) rkrow[bf][lane] = P[lane * R + k - r0];
     }
   };
   if (*status != 0) return;   // an earlier panel hit a zero pivot (every CTA sees it)
@@ -1331,34 +1343,30 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
     warp_argmax(best, bi);
     if (lane == 0) { cand_v[wid] = best; cand_i[wid] = bi; }
   }
-  cta_argmax();
+  cta_publish(0);
   cluster.sync();
 #pragma unroll
   for (int t = 0; t < KB; ++t) {
     if (t >= kb) break;
-    const int k = k0 + t;
+    const int k = k0 + t, bf = t & 1;
     if (tid < 32) {
       double best = -1.0;
       int bi = n;
       if (lane < C) {
-        best = *cluster.map_shared_rank(&cta_v, lane);
-        bi = *cluster.map_shared_rank(&cta_i, lane);
+        best = *cluster.map_shared_rank(&cta_v[bf], lane);
+        bi = *cluster.map_shared_rank(&cta_i[bf], lane);
       }
       warp_argmax(best, bi);
-      if (lane == 0) s_pr = bi < n ? bi : k;
+      const int pr = bi < n ? bi : k;
+      if (lane == 0) s_pr = pr;
+      // old pivot row: the winning CTA's candidate row (pr == k: old row k)
+      if (lane < kb) {
+        lk[lane] = *cluster.map_shared_rank(&rkrow[bf][lane], k / R);
+        lp[lane] = bi < n ? *cluster.map_shared_rank(&candrow[bf][lane], pr / R) : lk[lane];
+      }
     }
     __syncthreads();
     const int pr = s_pr;
-    if (tid < kb) {
-      if (pr >= r0 && pr < r1) pivrow[tid] = P[tid * R + pr - r0];
-      if (k >= r0 && k < r1) rkrow[tid] = P[tid * R + k - r0];
-    }
-    cluster.sync();   // (A) old pivot row and old row k published
-    if (tid < kb) {
-      lp[tid] = *cluster.map_shared_rank(&pivrow[tid], pr / R);
-      lk[tid] = *cluster.map_shared_rank(&rkrow[tid], k / R);
-    }
-    __syncthreads();
     double piv[KB], rk[KB];
 #pragma unroll
     for (int s2 = 0; s2 < KB; ++s2) {
@@ -1410,8 +1418,8 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
     }
     warp_argmax(nbest, nbi);
     if (lane == 0) { cand_v[wid] = nbest; cand_i[wid] = nbi; }
-    cta_argmax();
-    cluster.sync();   // (B) next candidates published; pivot rows read by all
+    if (t + 1 < kb) cta_publish(t + 1);
+    cluster.sync();   // next step's publication complete; this step's reads done
   }
   for (int e = tid; e < nr * kb; e += nt) {
     const int il = e / kb, t = e - il * kb;
