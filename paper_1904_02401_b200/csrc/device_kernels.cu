@@ -1345,9 +1345,11 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
   }
   cta_publish(0);
   cluster.sync();
-#pragma unroll
-  for (int t = 0; t < KB; ++t) {
-    if (t >= kb) break;
+  // the step loop stays rolled (an unrolled body of KB steps overflowed the
+  // instruction cache: "no instruction" was the top stall); column t is
+  // picked from the unrolled register rows by compare-and-select
+#pragma unroll 1
+  for (int t = 0; t < kb; ++t) {
     const int k = k0 + t, bf = t & 1;
     if (tid < 32) {
       double best = -1.0;
@@ -1373,7 +1375,8 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
       piv[s2] = s2 < kb ? lp[s2] : 0.0;
       rk[s2] = s2 < kb ? lk[s2] : 0.0;
     }
-    if (piv[t] == 0.0) {   // same value in every CTA: all leave together
+    const double pivt = lp[t];
+    if (pivt == 0.0) {     // same value in every CTA: all leave together
       if (cr == 0 && tid == 0) {
         perm[k] = pr;
         if (*status == 0) *status = k + 1;
@@ -1390,7 +1393,7 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
       src[k] = src[pr];
       src[pr] = a2;
     }
-    const double rp = 1.0 / piv[t];
+    const double rp = 1.0 / pivt;
     double nbest = -1.0;
     int nbi = n;
     for (int il = tid; il < nr; il += nt) {
@@ -1404,7 +1407,10 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
       double row[KB];
 #pragma unroll
       for (int s2 = 0; s2 < KB; ++s2) row[s2] = s2 < kb ? (i == pr ? rk[s2] : P[s2 * R + il]) : 0.0;
-      const double f = row[t];
+      double f = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < KB; ++s2)
+        if (s2 == t) f = row[s2];
 #pragma unroll
       for (int s2 = 0; s2 < KB; ++s2)
         if (s2 < kb) {
