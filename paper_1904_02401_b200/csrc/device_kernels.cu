@@ -2052,7 +2052,7 @@ bool gj_blocked_enabled() {
 
 // ALEFSI_GJ_CLUSTER (A/B only): CTAs per cluster panel; 0 = single-CTA
 // panel kernel.  Default: 16 (non-portable size, 2d config 0 39.5 -> 37 ms vs
-// 8) where the device can co-schedule it, else 8
+// 8) where the device can co-schedule it, else 8, else the single-CTA panel
 int gj_cluster_size() {
   static const int c = [] {
     const char* e = std::getenv("ALEFSI_GJ_CLUSTER");
@@ -2061,23 +2061,27 @@ int gj_cluster_size() {
                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute cat[1];
-    cat[0].id = cudaLaunchAttributeClusterDimension;
-    cat[0].val.clusterDim.x = 16;
-    cat[0].val.clusterDim.y = 1;
-    cat[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(16);
-    cfg.blockDim = dim3(256);
-    // the largest panel share: kGjMaxN rows over 16 CTAs
-    cfg.dynamicSmemBytes = (size_t)(kGjMaxN / 16) * 16 * 8 + (size_t)kGjMaxN * 4;
-    cfg.attrs = cat;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, gj_panel_cluster_kernel<16>,
-                                                   &cfg) == cudaSuccess && nclusters > 0;
-    cudaGetLastError();   // a refused query leaves no sticky error
-    return ok ? 16 : 8;
+    // largest cluster the device co-schedules with the largest panel share
+    // (kGjMaxN rows); none (e.g. no cluster support): single-CTA panels
+    for (int cs = 16; cs >= 8; cs /= 2) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute cat[1];
+      cat[0].id = cudaLaunchAttributeClusterDimension;
+      cat[0].val.clusterDim.x = cs;
+      cat[0].val.clusterDim.y = 1;
+      cat[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(cs);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = (size_t)(kGjMaxN / cs) * 16 * 8 + (size_t)kGjMaxN * 4;
+      cfg.attrs = cat;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, gj_panel_cluster_kernel<16>,
+                                                     &cfg) == cudaSuccess && nclusters > 0;
+      cudaGetLastError();   // a refused query leaves no sticky error
+      if (ok) return cs;
+    }
+    return 0;
   }();
   return c;
 }
