@@ -1369,12 +1369,6 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
     }
     __syncthreads();
     const int pr = s_pr;
-    double piv[KB], rk[KB];
-#pragma unroll
-    for (int s2 = 0; s2 < KB; ++s2) {
-      piv[s2] = s2 < kb ? lp[s2] : 0.0;
-      rk[s2] = s2 < kb ? lk[s2] : 0.0;
-    }
     const double pivt = lp[t];
     if (pivt == 0.0) {     // same value in every CTA: all leave together
       if (cr == 0 && tid == 0) {
@@ -1396,31 +1390,26 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
     const double rp = 1.0 / pivt;
     double nbest = -1.0;
     int nbi = n;
+    // rows streamed element by element (old pivot row and old row k from
+    // shared memory): the same expressions as gj_panel_kernel, few registers
     for (int il = tid; il < nr; il += nt) {
       const int i = r0 + il;
       if (i == k) {
-#pragma unroll
-        for (int s2 = 0; s2 < KB; ++s2)
-          if (s2 < kb) P[s2 * R + il] = (s2 == t) ? rp : piv[s2] * rp;
+        for (int s2 = 0; s2 < kb; ++s2) P[s2 * R + il] = (s2 == t) ? rp : lp[s2] * rp;
         continue;
       }
-      double row[KB];
-#pragma unroll
-      for (int s2 = 0; s2 < KB; ++s2) row[s2] = s2 < kb ? (i == pr ? rk[s2] : P[s2 * R + il]) : 0.0;
-      double f = 0.0;
-#pragma unroll
-      for (int s2 = 0; s2 < KB; ++s2)
-        if (s2 == t) f = row[s2];
-#pragma unroll
-      for (int s2 = 0; s2 < KB; ++s2)
-        if (s2 < kb) {
-          const double v = (s2 == t) ? -f * rp : row[s2] - f * (piv[s2] * rp);
-          P[s2 * R + il] = v;
-          if (s2 == t + 1 && i > k) {
-            const double a = fabs(v);
-            if (a > nbest) { nbest = a; nbi = i; }
-          }
+      const bool isp = i == pr;
+      const double f = isp ? lk[t] : P[t * R + il];
+#pragma unroll 4
+      for (int s2 = 0; s2 < kb; ++s2) {
+        const double old = isp ? lk[s2] : P[s2 * R + il];
+        const double v = (s2 == t) ? -f * rp : old - f * (lp[s2] * rp);
+        P[s2 * R + il] = v;
+        if (s2 == t + 1 && i > k) {
+          const double a = fabs(v);
+          if (a > nbest) { nbest = a; nbi = i; }
         }
+      }
     }
     warp_argmax(nbest, nbi);
     if (lane == 0) { cand_v[wid] = nbest; cand_i[wid] = nbi; }
@@ -1480,14 +1469,15 @@ __global__ void __launch_bounds__(256) gj_panel_cluster_kernel(double* M, int n,
 // gj_panel_kernel).  CTA tile: 32 rows x 128 columns, thread = one column x
 // 16 rows (coalesced row segments); the tile's permutation sources, panel
 // coefficients and pivot-row segments are staged in shared memory.
+template <int KBM>
 __global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0, int kb,
                                                         const int* __restrict__ src,
                                                         const double* __restrict__ slab,
                                                         const int* __restrict__ rowslot,
                                                         const int64_t* status) {
-  __shared__ double sK[16][128];
-  __shared__ double cf[32][17];
-  __shared__ int kslot[16], rsrc[32];
+  __shared__ double sK[KBM][128];
+  __shared__ double cf[32][KBM + 1];
+  __shared__ int kslot[KBM], rsrc[32];
   if (*status != 0) return;
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 128, tid = threadIdx.x;
   if (tid < kb) kslot[tid] = rowslot[src[k0 + tid]];
@@ -1510,9 +1500,9 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0
   const int jj = tid & 127, j = j0 + jj;
   if (j >= n || (j >= k0 && j < k0 + kb)) return;
   // this thread's column of the pivot-row segments, reused for its 16 rows
-  double sk[16];
+  double sk[KBM];
 #pragma unroll
-  for (int s2 = 0; s2 < 16; ++s2) sk[s2] = s2 < kb ? sK[s2][jj] : 0.0;
+  for (int s2 = 0; s2 < KBM; ++s2) sk[s2] = s2 < kb ? sK[s2][jj] : 0.0;
 #pragma unroll 4
   for (int r = tid >> 7; r < 32; r += 2) {
     const int i = i0 + r;
@@ -1520,7 +1510,7 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0
     const int rs = rsrc[r];
     double acc = rs == -2 ? 0.0 : (rs == -1 ? M[(int64_t)i * n + j] : slab[(int64_t)rs * n + j]);
 #pragma unroll
-    for (int s2 = 0; s2 < 16; ++s2)
+    for (int s2 = 0; s2 < KBM; ++s2)
       if (s2 < kb) acc = fma(cf[r][s2], sk[s2], acc);
     M[(int64_t)i * n + j] = acc;
   }
@@ -2072,7 +2062,7 @@ int gj_cluster_size() {
       cat[0].val.clusterDim.z = 1;
       cfg.gridDim = dim3(cs);
       cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = (size_t)(kGjMaxN / cs) * 16 * 8 + (size_t)kGjMaxN * 4;
+      cfg.dynamicSmemBytes = (size_t)(kGjMaxN / cs) * 32 * 8 + (size_t)kGjMaxN * 4;
       cfg.attrs = cat;
       cfg.numAttrs = 1;
       int nclusters = 0;
@@ -2087,10 +2077,20 @@ int gj_cluster_size() {
 }
 bool gj_cluster_enabled() { return gj_cluster_size() > 0; }
 
+// ALEFSI_GJ_KB=32 (A/B only): 32-column cluster panels — half the update
+// passes, but slower overall (config 2 18.2 -> 18.9 ms, config 1 50.3 -> 51.6)
+int gj_cluster_kb() {
+  static const int v = [] {
+    const char* e = std::getenv("ALEFSI_GJ_KB");
+    return e != nullptr && std::atoi(e) == 32 ? 32 : 16;
+  }();
+  return v;
+}
+
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s) {
   // cluster panels: the n x 16 panel spread over 8-16 SMs fits for every n <= kGjMaxN
-  const bool clus = gj_blocked_enabled() && gj_cluster_enabled() && n >= 64;
-  const int nb = clus ? 16 : gj_blocked_enabled() ? gj_panel_width(n) : 0;
+  const bool clus = gj_blocked_enabled() && gj_cluster_enabled() && n >= 128;
+  const int nb = clus ? gj_cluster_kb() : gj_blocked_enabled() ? gj_panel_width(n) : 0;
   if (nb > 0 && n <= kGjMaxN) {
     // work: perm (n int64) | src (n int) | rowslot (n int) | slab (2 nb x n)
     int64_t* perm = reinterpret_cast<int64_t*>(work);
@@ -2113,11 +2113,15 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
     const dim3 ug((unsigned)grid_for(n, 128), (unsigned)grid_for(n, 32));
     const int kGjCluster = gj_cluster_size() > 0 ? gj_cluster_size() : 8;   // CTAs per panel
     const int R = (int)((n + kGjCluster - 1) / kGjCluster);
-    const size_t csmem = (size_t)R * 16 * 8 + (size_t)n * 4;
+    const size_t csmem = (size_t)R * nb * 8 + (size_t)n * 4;
     static bool cattr = [] {
       cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
       cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(gj_panel_cluster_kernel<32>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
+      cudaFuncSetAttribute(gj_panel_cluster_kernel<32>,
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       return true;
     }();
@@ -2136,7 +2140,10 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
     cfg.numAttrs = 1;
     for (int64_t k0 = 0; k0 < n; k0 += nb) {
       const int kb = (int)std::min<int64_t>(nb, n - k0);
-      if (clus)
+      if (clus && nb == 32)
+        cudaLaunchKernelEx(&cfg, gj_panel_cluster_kernel<32>, M, (int)n, (int)k0, kb, R, perm, src,
+                           slab, rowslot, status);
+      else if (clus)
         cudaLaunchKernelEx(&cfg, gj_panel_cluster_kernel<16>, M, (int)n, (int)k0, kb, R, perm, src,
                            slab, rowslot, status);
       else if (nb == 16)
@@ -2148,7 +2155,12 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
       else
         gj_panel_kernel<4><<<1, 512, smem, s>>>(M, (int)n, (int)k0, kb, perm, src, slab,
                                                 rowslot, status);
-      gj_update_kernel<<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot, status);
+      if (nb == 32)
+        gj_update_kernel<32><<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot,
+                                                status);
+      else
+        gj_update_kernel<16><<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot,
+                                                status);
     }
     gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm, status);
     return 0;

@@ -58,7 +58,7 @@ void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_
 // ---- coarse level: dense inverse and apply
 // work: dense_inverse_work(n) doubles
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s);
-inline int64_t dense_inverse_work(int64_t n) { return 2 * n + 2 + 32 * n; }
+inline int64_t dense_inverse_work(int64_t n) { return 2 * n + 2 + 64 * n; }
 void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
                          cudaStream_t s);
 
