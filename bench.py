@@ -40,6 +40,61 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# ------------------------------------------------------------------------- parity gate
+class ParityError(RuntimeError):
+    """The solve about to be timed does not reproduce the committed golden."""
+
+
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def golden_for(workload):
+    """Committed golden of a workload's full-size solve: the reference's own
+    run (tests/golden/<w>.json) where the reference could run it, else the
+    pinned CPU oracle's (tests/golden/<w>_oracle.json)."""
+    for name in (f"{workload}.json", f"{workload}_oracle.json"):
+        path = os.path.join(GOLDEN_DIR, name)
+        if os.path.exists(path):
+            with open(path) as f:
+                g = json.load(f)
+            if "residuals" in g:
+                return path, g
+    return None, None
+
+
+def check_against_golden(workload, iterations, residuals, x_checksums,
+                         hist_tol=1e-10, x_tol=1e-9):
+    """north_star's parity bar on the solve bench.py times: identical
+    iteration count, residual history within 1e-10 relative, solution
+    checksums within 1e-9.  Raises ParityError otherwise."""
+    path, g = golden_for(workload)
+    if g is None:
+        raise ParityError(f"no committed golden history for workload {workload}")
+    rel = os.path.relpath(path, ROOT)
+    if iterations != g["iterations"] or len(residuals) != len(g["residuals"]):
+        raise ParityError(f"{workload}: {iterations} GMRES iterations, golden {rel} has "
+                          f"{g['iterations']}")
+    r, rr = np.asarray(residuals, dtype=float), np.asarray(g["residuals"], dtype=float)
+    hist = float(np.max(np.abs(r - rr) / rr))
+    if not hist < hist_tol:
+        raise ParityError(f"{workload}: residual history differs from {rel} by {hist:.3e}")
+    xrel = None
+    if x_checksums is not None:
+        c, cc = np.asarray(x_checksums), np.asarray(g["x_checksums"])
+        xrel = float(np.max(np.abs(c - cc) / np.abs(cc)))
+        if not xrel <= x_tol:
+            raise ParityError(f"{workload}: solution checksums differ from {rel} by {xrel:.3e}")
+    return {"source": rel, "iterations": int(g["iterations"]),
+            "max_rel_history_diff": hist, "max_rel_checksum_diff": xrel}
+
+
+def vector_checksums(x):
+    """tests/golden_util.vector_checksums (norm + two seeded projections)."""
+    rng = np.random.default_rng(99)
+    ps = [rng.standard_normal(len(x)) for _ in range(2)]
+    return [float(np.linalg.norm(x))] + [float(p @ x) for p in ps]
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -197,6 +252,10 @@ def run_ours(args, rank, world):
         _, st = solve()
     iterations = st.iterations
     log(f"[rank {rank}] warm-up done: {iterations} GMRES iterations")
+    # parity gate: the solve about to be timed must reproduce the golden
+    parity = check_against_golden(args.workload, st.iterations, st.residuals,
+                                  vector_checksums(x_dev.cpu().numpy()))
+    log(f"[rank {rank}] parity vs {parity['source']}: history {parity['max_rel_history_diff']:.1e}")
 
     def barrier():
         if world > 1:
@@ -289,7 +348,7 @@ def run_ours(args, rank, world):
     cnt, ms = prof[(dom, True)]
     avg_ms = ms / (cnt / per_app[dom])
     achieved = kb[dom] / (avg_ms * 1e-3) / 1e9
-    traffic = ncu_traffic(dom)
+    traffic = ncu_traffic(args.workload, dom)
     n = len(case.b)
     solves_per_s = whole_job_rate(args.steps, world, ms_total)
     out = {
@@ -297,13 +356,9 @@ def run_ours(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded sine-mode linearisation state and RHS, BASELINE config 3)",
-        "config": {"workload": args.workload, "fine_mesh": "x".join(map(str, wl.fine_cells)),
-                   "levels": wl.n_levels, "dofs": n,
-                   "vanka_block": "x".join([str(case.patches[-1].sizes()[0])] * 2),
-                   "nu_pre": wl.nu_pre, "nu_post": wl.nu_post, "omega": wl.omega,
-                   "rel_tol": wl.rel_tol, "gmres_iterations": iterations,
-                   "l2": "inputs larger than L2 (finest operator + inverses > 20 GB)",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "config": workload_config(wl, n, iterations, case.patches[-1].sizes(),
+                                  kb["spmv"] + kb["vanka_apply"], world),
+        "parity": parity,
         "e2e": {"value": world * args.steps / (ms_e2e * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8 + 8 * (iterations + 1)},
         "gpu_launches": launches,
@@ -333,12 +388,44 @@ def run_ours(args, rank, world):
     return out
 
 
-def ncu_traffic(kind):
+def ncu_traffic(workload, kind):
+    """dram__bytes_read+write of one launch of ``kind`` on ``workload``'s
+    finest level, from an ncu --set full capture of that workload
+    (profiles/ncu_traffic.json, keyed workload -> kernel); None when no
+    capture of that workload/kernel exists."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as f:
-        return json.load(f).get(kind)
+        rec = json.load(f).get(workload) or {}
+    v = rec.get(kind)
+    return float(v) if v is not None else None
+
+
+L2_BYTES = 126 * 2 ** 20
+
+
+def workload_config(wl, n, iterations, sizes, finest_bytes, world):
+    """``config`` of the JSON line; identical in both arms (same_config)."""
+    lo, hi = wl.solid_box()
+    fs, ss = wl.patch_strategies()
+    cfg = {"workload": wl.name, "fine_mesh": "x".join(map(str, wl.fine_cells)),
+           "levels": wl.n_levels, "dofs": n,
+           "vanka_block": "x".join([str(sizes[0])] * 2),
+           "nu_pre": wl.nu_pre, "nu_post": wl.nu_post, "omega": wl.omega,
+           "rel_tol": wl.rel_tol, "gmres_iterations": iterations,
+           "l2": (f"inputs larger than L2: one finest-level SpMV + Vanka apply stream "
+                  f"{finest_bytes / 1e9:.2f} GB > {L2_BYTES / 2 ** 20:.0f} MiB L2, no flush"
+                  if finest_bytes > L2_BYTES else
+                  f"finest level {finest_bytes / 1e6:.0f} MB fits the {L2_BYTES / 2 ** 20:.0f} MiB L2"),
+           "deviations": {
+               "solid_box": f"{[float(v) for v in lo]}..{[float(v) for v in hi]} (BASELINE [1,2]x[0.4,0.6]^{wl.dim - 1}, "
+                            f"snapped outward to 1/8; DESIGN.md)",
+               "lps_dt": wl.dt,
+               "deform_taper": wl.deform_taper,
+               "patches": f"fluid={fs}, solid={ss}"},
+           "parallelism": "replicas" if world > 1 else "single GPU"}
+    return cfg
 
 
 # ------------------------------------------------------------------ CPU oracle baseline

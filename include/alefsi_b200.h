@@ -14,6 +14,18 @@
  * Index conventions follow the reference: a level's dofs are node-major,
  * dof = node * nc + component with nc = dim + 1 (p, v_1..v_d); level 0 is
  * the coarsest level.
+ *
+ * Hard limits (violations return ALEFSI_ERR_ARG with a message):
+ *   - GMRES max_iter in [1, 510] (Hessenberg columns staged in 512-entry
+ *     shared arrays of the Krylov kernels);
+ *   - coarsest level at most 4096 dofs (dense explicit inverse, one n x 16
+ *     panel per cluster of CTAs);
+ *   - Vanka patch sizes with compiled kernels: nc = 3 with 27 / 75 / 81 dofs
+ *     per patch, nc = 4 with 108 / 500, nc = 2 with 18 (2D/3D Q2 one-element
+ *     and 2x2(x2)-cell macro patches of the reference's PatchSet);
+ *   - device assembly (asm_*): fewer than 2^31 blocks per level, dim 2 or 3,
+ *     nq == 3^dim Gauss points; the shape tables of one dim are loaded once
+ *     per process and later calls must pass the same tables.
  */
 #ifndef ALEFSI_B200_H
 #define ALEFSI_B200_H
@@ -112,7 +124,9 @@ int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t n
  * colour (group_kind 0 fluid / 1 solid; a colour's cells share no node), the
  * LPS macro entries as (cell slot | -1, pp slot | -1, value) triples
  * (problem.py:79-90) and the Dirichlet row mask (n_nodes*nc bytes).
- * asm_tables: Q2 basis N (nq,nb), gradients dN (nq,nb,dim), weights (nq).
+ * asm_tables: Q2 basis N (nq,nb), gradients dN (nq,nb,dim), weights (nq);
+ * nq must equal nb = 3^dim; one constant bank per dim, loaded by the first
+ * call for that dim (later calls must pass identical tables).
  * asm_momentum: params = {rho_f, mu_f, rho_s, mu_s, lam_s, k, theta}; U and
  * U_prev host (n_nodes, 1+2dim); extra = host-reduced outflow-facet blocks
  * (unique slots; pass n_extra = 0 once asm_outflow has been called for the
@@ -182,7 +196,9 @@ int alefsi_mg_set_constrained(alefsi_mg h, int32_t level, const uint8_t* mask);
 
 /* VankaSmoother.factorize / patch_factorize on every level >= 1 and the
  * coarse-level factorisation of MgSolver.__init__ (reference
- * linsolve.py:120-134, 163-165, 236). */
+ * linsolve.py:120-134, 163-165, 236).  Coarsest level <= 4096 dofs;
+ * ALEFSI_ERR_SINGULAR names the first singular patch (or the coarse
+ * block).  Scratch is kept in the handle across re-factorisations. */
 int alefsi_mg_factorize(alefsi_mg h);
 
 /* z = one V-cycle applied to b (MgSolver.dot, reference linsolve.py:238-255). */
@@ -216,7 +232,8 @@ int alefsi_mg_info(alefsi_mg h, int32_t level, int64_t* info);
 /* Right-preconditioned, unrestarted GMRES with the V-cycle as
  * preconditioner (gmres, reference linsolve.py:41-115): classical
  * Gram-Schmidt with the conditional second pass, Givens rotations,
- * residuals[0..iterations] = the reference's stats.residuals.  Returns
+ * residuals[0..iterations] = the reference's stats.residuals (max_iter + 1
+ * doubles).  max_iter must be in [1, 510].  Returns
  * ALEFSI_ERR_NOT_CONVERGED (x and residuals still written) when max_iter is
  * reached above tolerance. */
 int alefsi_gmres(alefsi_mg h, const double* b, double* x, double rel_tol, double abs_tol,

@@ -10,16 +10,21 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 #include "assembly_kernels.cuh"
 
 namespace alefsi {
 namespace {
 
+// Q2 shape tables at the Gauss points, one constant bank per dimension
+// (bank D == 3): a 2D and a 3D hierarchy can be assembled in the same
+// process; each bank is written once (set_assembly_tables) and later calls
+// must pass identical tables, so no bank is ever rewritten while in use.
 constexpr int kMaxQ = 27, kMaxB = 27;
-__constant__ double cN[kMaxQ * kMaxB];          // N[q][b]
-__constant__ double cdN[kMaxQ * kMaxB * 3];     // dN[q][b][j]
-__constant__ double cW[kMaxQ];                  // Gauss weights
+__constant__ double cN[2][kMaxQ * kMaxB];          // N[q][b]
+__constant__ double cdN[2][kMaxQ * kMaxB * 3];     // dN[q][b][j]
+__constant__ double cW[2][kMaxQ];                  // Gauss weights
 
 template <int D>
 __device__ __forceinline__ double det(const double (&A)[D][D]) {
@@ -105,7 +110,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         double acc = 0.0;
-        for (int b = 0; b < NB; ++b) acc += sh.X[b][i] * cdN[(q * NB + b) * 3 + j];
+        for (int b = 0; b < NB; ++b) acc += sh.X[b][i] * cdN[D == 3][(q * NB + b) * 3 + j];
         J[i][j] = acc;
       }
     const double dt = det<D>(J);
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
     for (int i = 0; i < D; ++i)
 #pragma unroll
       for (int j = 0; j < D; ++j) sh.Jinv[q][i * D + j] = Ji[i][j];
-    sh.s[q][5] = dt * cW[q];
+    sh.s[q][5] = dt * cW[D == 3][q];
   }
   __syncthreads();
   for (int t = tid; t < NQ * NB; t += blockDim.x) {
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
     for (int i = 0; i < D; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < D; ++j) acc += cdN[(q * NB + b) * 3 + j] * sh.Jinv[q][j * D + i];
+      for (int j = 0; j < D; ++j) acc += cdN[D == 3][(q * NB + b) * 3 + j] * sh.Jinv[q][j * D + i];
       sh.G[q][b][i] = acc;
     }
   }
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
       for (int j = 0; j < D; ++j) gv[i][j] = gu[i][j] = gvp[i][j] = gup[i][j] = 0.0;
     }
     for (int b = 0; b < NB; ++b) {
-      const double nb = cN[q * NB + b];
+      const double nb = cN[D == 3][q * NB + b];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         v[i] += nb * sh.U[b][1 + i];
@@ -295,7 +300,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
       for (int j = 0; j < NC; ++j) blk[i][j] = 0.0;
     double diag = 0.0;
     for (int q = 0; q < NQ; ++q) {
-      const double nb = cN[q * NB + b], na = cN[q * NB + c];
+      const double nb = cN[D == 3][q * NB + b], na = cN[D == 3][q * NB + c];
       if constexpr (KIND == 0) {
         double gkg = 0.0;
 #pragma unroll
@@ -371,19 +376,19 @@ __global__ void __launch_bounds__(128) residual_cells_kernel(ResArgs a, const in
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         double acc = 0.0;
-        for (int b = 0; b < NB; ++b) acc += cdN[(q * NB + b) * 3 + j] * X[b][i];
+        for (int b = 0; b < NB; ++b) acc += cdN[D == 3][(q * NB + b) * 3 + j] * X[b][i];
         J[i][j] = acc;
       }
     const double dt = det<D>(J);
     if (!(dt > 0.0)) bad = 1;
     inv<D>(J, Ji, dt);
-    wq[q] = dt * cW[q];
+    wq[q] = dt * cW[D == 3][q];
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < D; ++j) acc += cdN[(q * NB + b) * 3 + j] * Ji[j][i];
+        for (int j = 0; j < D; ++j) acc += cdN[D == 3][(q * NB + b) * 3 + j] * Ji[j][i];
         G[q][b][i] = acc;
       }
   }
@@ -401,7 +406,7 @@ __global__ void __launch_bounds__(128) residual_cells_kernel(ResArgs a, const in
       for (int j = 0; j < D; ++j) gv[i][j] = gu[i][j] = gvp[i][j] = gup[i][j] = 0.0;
     }
     for (int b = 0; b < NB; ++b) {
-      const double nb = cN[q * NB + b];
+      const double nb = cN[D == 3][q * NB + b];
       p += nb * U[b][0];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
@@ -583,7 +588,7 @@ __global__ void __launch_bounds__(128) residual_cells_kernel(ResArgs a, const in
     const int b = t / NO, f = t - b * NO;
     double acc = 0.0;
     for (int q = 0; q < NQ; ++q) {
-      double s = cN[q * NB + b] * val[q][f];
+      double s = cN[D == 3][q * NB + b] * val[q][f];
 #pragma unroll
       for (int j = 0; j < D; ++j) s += G[q][b][j] * grd[q][f][j];
       acc += wq[q] * s;
@@ -818,15 +823,39 @@ __global__ void dirichlet_kernel(double* data, int nc, double* pp, int64_t n_nod
 
 }  // namespace
 
-void set_assembly_tables(const double* N, const double* dN, const double* w, int nq, int nb,
-                         int dim) {
-  static double hdN[kMaxQ * kMaxB * 3];
-  for (int q = 0; q < nq; ++q)
-    for (int b = 0; b < nb; ++b)
-      for (int j = 0; j < 3; ++j) hdN[(q * nb + b) * 3 + j] = j < dim ? dN[(q * nb + b) * dim + j] : 0.0;
-  cudaMemcpyToSymbol(cN, N, sizeof(double) * nq * nb);
-  cudaMemcpyToSymbol(cdN, hdN, sizeof(double) * nq * nb * 3);
-  cudaMemcpyToSymbol(cW, w, sizeof(double) * nq);
+int set_assembly_tables(const double* N, const double* dN, const double* w, int nq, int nb,
+                        int dim) {
+  static bool loaded[2] = {false, false};
+  static double hN[2][kMaxQ * kMaxB], hdN[2][kMaxQ * kMaxB * 3], hW[2][kMaxQ];
+  if (nq != nb || nb > kMaxB || (dim != 2 && dim != 3)) return 1;
+  const int bank = dim == 3;
+  double tN[kMaxQ * kMaxB], tdN[kMaxQ * kMaxB * 3] = {0}, tW[kMaxQ];
+  for (int q = 0; q < nq; ++q) {
+    tW[q] = w[q];
+    for (int b = 0; b < nb; ++b) {
+      tN[q * nb + b] = N[q * nb + b];
+      for (int j = 0; j < 3; ++j)
+        tdN[(q * nb + b) * 3 + j] = j < dim ? dN[(q * nb + b) * dim + j] : 0.0;
+    }
+  }
+  if (loaded[bank]) {
+    const bool same = std::memcmp(tN, hN[bank], sizeof(double) * nq * nb) == 0 &&
+                      std::memcmp(tdN, hdN[bank], sizeof(double) * nq * nb * 3) == 0 &&
+                      std::memcmp(tW, hW[bank], sizeof(double) * nq) == 0;
+    return same ? 0 : 2;
+  }
+  std::memcpy(hN[bank], tN, sizeof(double) * nq * nb);
+  std::memcpy(hdN[bank], tdN, sizeof(double) * nq * nb * 3);
+  std::memcpy(hW[bank], tW, sizeof(double) * nq);
+  const size_t o = (size_t)bank;
+  if (cudaMemcpyToSymbol(cN, tN, sizeof(double) * nq * nb, o * sizeof(double) * kMaxQ * kMaxB) !=
+          cudaSuccess ||
+      cudaMemcpyToSymbol(cdN, tdN, sizeof(double) * nq * nb * 3,
+                         o * sizeof(double) * kMaxQ * kMaxB * 3) != cudaSuccess ||
+      cudaMemcpyToSymbol(cW, tW, sizeof(double) * nq, o * sizeof(double) * kMaxQ) != cudaSuccess)
+    return 3;
+  loaded[bank] = true;
+  return 0;
 }
 
 void launch_assemble_cells(const AsmArgs& a, int dim, int kind, const int32_t* cells,

@@ -66,8 +66,10 @@ void launch_residual_cells(const ResArgs& a, int dim, int kind, const int32_t* c
                            int64_t n_cells, double* out, cudaStream_t s);
 
 // Q2 tables at the Gauss points: N (nq, nb), dN (nq, nb, dim), weights (nq)
-void set_assembly_tables(const double* N, const double* dN, const double* w, int nq, int nb,
-                         int dim);
+// 0 ok; 1 bad shape (nq != nb or dim not 2/3); 2 tables differ from those
+// already loaded for this dim; 3 CUDA error
+int set_assembly_tables(const double* N, const double* dN, const double* w, int nq, int nb,
+                        int dim);
 // kind 0: fluid cells, 1: solid cells; cells of one colour (no shared nodes)
 void launch_assemble_cells(const AsmArgs& a, int dim, int kind, const int32_t* cells,
                            int64_t n_cells, cudaStream_t s);

@@ -18,8 +18,6 @@
 
 namespace alefsi {
 
-bool small_level_kernels_enabled();
-
 namespace {
 
 constexpr int kWarp = 32;
@@ -207,13 +205,16 @@ __device__ __forceinline__ d4 ld256_ro(const double* p) {       // read-only pat
 // row and the 32-byte x block with one instruction each (half the load
 // instructions of spmv32_kernel; same FMA order, bitwise-equal results).
 //
+// Block columns are fetched 32 at a time with one coalesced load and handed
+// out by shuffle, so the x gather of an iteration waits on L2 only.
+//
 // UNR: the four column steps of a 32-block chunk are unrolled so their loads
 // are in flight together.  Used on small, L2-resident levels, where a
 // warp's chain of dependent L2 round trips (not resident warps) sets the
 // time; the large levels keep one step at a time for 32 registers and full
 // occupancy.  Same FMA order either way: bitwise-equal results.
-template <int MODE, bool SHFL, bool UNR = false>
-__global__ void __launch_bounds__(256) spmv4_v4_kernel(int64_t n, const int64_t* __restrict__ indptr,
+template <int MODE, bool UNR = false>
+__global__ void __launch_bounds__(256) spmv4_kernel(int64_t n, const int64_t* __restrict__ indptr,
                                                        const int32_t* __restrict__ indices,
                                                        const double* __restrict__ data,
                                                        const int64_t* __restrict__ pp_ptr,
@@ -230,20 +231,7 @@ __global__ void __launch_bounds__(256) spmv4_v4_kernel(int64_t n, const int64_t*
   const int beg = (int)indptr[row], end = (int)indptr[row + 1];
   const double* dr = data + r * NC;
   double acc = 0.0;
-  if constexpr (!SHFL) {
-    for (int blk = beg + sub; blk < end; blk += BPI) {
-      const int col = __ldcs(indices + blk);
-      const d4 vv = ld256_stream(dr + blk * (NC * NC));
-      const d4 xx = ld256_ro(x + col * NC);
-      acc = fma(vv.x, xx.x, acc);
-      acc = fma(vv.y, xx.y, acc);
-      acc = fma(vv.z, xx.z, acc);
-      acc = fma(vv.w, xx.w, acc);
-    }
-  }
-  // SHFL: block columns are fetched 32 at a time with one coalesced load and
-  // handed out by shuffle, so the x gather of an iteration waits on L2 only
-  if constexpr (SHFL) for (int base = beg; base < end; base += kWarp) {
+  for (int base = beg; base < end; base += kWarp) {
     const int cidx = base + lane < end ? __ldcs(indices + base + lane) : 0;
 #pragma unroll (UNR ? 4 : 1)
     for (int j = 0; j < kWarp / BPI; ++j) {
@@ -763,12 +751,20 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
 }
 
 // --------------------------------------------------------------------------
-// Large patches (2x2x2-cell macros in 3D: 500 x 500): batched Gauss-Jordan
-// in global memory, one pivot step per launch pair over all patches of the
-// group, same implicit pivoting and output mapping as the register kernel.
+// Large patches (2x2x2-cell macros in 3D: 500 x 500, the reference's default
+// solid blocking, newton.py:53-56): batched blocked Gauss-Jordan.  Each patch
+// matrix is gathered row-major into its own slot of the group's inverse
+// storage (ld == np), then every 16-column panel is factorised by one CTA per
+// patch (gj_panel_kernel, panel in shared memory) and applied to the rest of
+// all patches' matrices by one 3D-grid gj_update_kernel launch; the row
+// permutation is undone (gj_unscramble_kernel) and each inverse transposed in
+// place to the column-major storage of the apply kernels.  Pivot choice of
+// partial pivoting (largest |value| among the remaining rows, reference
+// linsolve.py:131 np.linalg.inv -> getrf); ~64 launches per factorisation
+// instead of one launch pair per pivot step.
 // --------------------------------------------------------------------------
 __global__ void big_gather_kernel(DevMatrix A, int np_, int npn, const int32_t* nodes,
-                                  double* M, int* used) {
+                                  double* M) {
   const int64_t p = blockIdx.y;
   const int32_t* pn = nodes + p * npn;
   double* Mp = M + p * (int64_t)np_ * np_;
@@ -798,96 +794,27 @@ __global__ void big_gather_kernel(DevMatrix A, int np_, int npn, const int32_t* 
     }
     Mp[e] = v;
   }
-  if (blockIdx.x == 0)
-    for (int i = threadIdx.x; i < np_; i += blockDim.x) used[p * np_ + i] = 0;
 }
 
-// pivot of step k for patch blockIdx.x: publish column k and the scaled row
-__global__ void __launch_bounds__(512) big_pivot_kernel(int np_, int k, double* M, int* used,
-                                                        int* perm, double* colk, double* prow,
-                                                        int64_t* status) {
-  __shared__ double sb[16];
-  __shared__ int si[16];
-  __shared__ int prs;
-  const int64_t p = blockIdx.x;
-  double* Mp = M + p * (int64_t)np_ * np_;
-  int* up = used + p * np_;
-  double best = -1.0;
-  int bi = np_;
-  for (int r = threadIdx.x; r < np_; r += blockDim.x) {
-    const double v = Mp[(int64_t)r * np_ + k];
-    colk[p * np_ + r] = v;
-    const double a = up[r] ? -1.0 : fabs(v);
-    if (a > best) { best = a; bi = r; }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-  }
-  if ((threadIdx.x & 31) == 0) { sb[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int nw = blockDim.x >> 5;
-    best = threadIdx.x < nw ? sb[threadIdx.x] : -2.0;
-    bi = threadIdx.x < nw ? si[threadIdx.x] : np_;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    if (threadIdx.x == 0) {
-      prs = bi;
-      up[bi] = 1;
-      perm[p * np_ + k] = bi;
-    }
-  }
-  __syncthreads();
-  const int pr = prs;
-  const double piv = Mp[(int64_t)pr * np_ + k];
-  if (piv == 0.0) {
-    if (threadIdx.x == 0) atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
-                                    (unsigned long long)(p + 1));
+// row-major inverse -> column-major (in place, n x n per patch); a failed
+// patch reports 1 + its index in the group status (first one wins)
+__global__ void big_finish_kernel(int np_, double* M, const int64_t* pstatus, int64_t* status) {
+  const int64_t p = blockIdx.y;
+  if (pstatus[p] != 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
+                (unsigned long long)(p + 1));
     return;
   }
-  const double rp = 1.0 / piv;
-  for (int c = threadIdx.x; c < np_; c += blockDim.x) {
-    const double v = (c == k) ? rp : Mp[(int64_t)pr * np_ + c] * rp;
-    prow[p * np_ + c] = v;
-    Mp[(int64_t)pr * np_ + c] = v;
-  }
-}
-
-__global__ void big_eliminate_kernel(int np_, int k, double* M, const int* perm,
-                                     const double* colk, const double* prow) {
-  const int64_t p = blockIdx.y;
   double* Mp = M + p * (int64_t)np_ * np_;
-  const int pr = perm[p * np_ + k];
-  const double rp = prow[p * np_ + k];
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)np_ * np_;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / np_), c = (int)(e - (int64_t)r * np_);
-    if (r == pr) continue;
-    const double f = colk[p * np_ + r];
-    Mp[e] = (c == k) ? -f * rp : fma(-f, prow[p * np_ + c], Mp[e]);
-  }
-}
-
-__global__ void big_finalize_kernel(int np_, int ld, const double* M, const int* perm,
-                                    double* inv) {
-  const int64_t p = blockIdx.y;
-  const double* Mp = M + p * (int64_t)np_ * np_;
-  const int* pp = perm + p * np_;
-  extern __shared__ int step_of_row[];
-  for (int k = threadIdx.x; k < np_; k += blockDim.x) step_of_row[pp[k]] = k;
-  __syncthreads();
-  double* out = inv + p * (int64_t)np_ * ld;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)np_ * np_;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / np_), c = (int)(e - (int64_t)r * np_);
-    out[(int64_t)pp[c] * ld + step_of_row[r]] = Mp[e];
+    const int i = (int)(e / np_), j = (int)(e - (int64_t)i * np_);
+    if (i < j) {
+      const double t = Mp[e];
+      Mp[e] = Mp[(int64_t)j * np_ + i];
+      Mp[(int64_t)j * np_ + i] = t;
+    }
   }
 }
 
@@ -1124,6 +1051,15 @@ __global__ void __launch_bounds__(512) gj_panel_kernel(double* M, int n, int k0,
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
   };
+  {   // batched use (Vanka macro patches): matrix blockIdx.x of a batch
+    const int64_t bat = blockIdx.x;
+    M += bat * n * n;
+    perm += bat * n;
+    src_out += bat * n;
+    rowslot += bat * n;
+    slab += bat * 2 * KB * n;
+    status += bat;
+  }
   if (*status != 0) return;   // an earlier panel hit a zero pivot
   for (int e = tid; e < n * kb; e += nt) {
     const int i = e / kb, t = e - i * kb;
@@ -1478,6 +1414,14 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0
   __shared__ double sK[KBM][128];
   __shared__ double cf[32][KBM + 1];
   __shared__ int kslot[KBM], rsrc[32];
+  {   // batched use: matrix blockIdx.z
+    const int64_t bat = blockIdx.z;
+    M += bat * n * n;
+    src += bat * n;
+    rowslot += bat * n;
+    slab += bat * 2 * KBM * n;
+    status += bat;
+  }
   if (*status != 0) return;
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 128, tid = threadIdx.x;
   if (tid < kb) kslot[tid] = rowslot[src[k0 + tid]];
@@ -1519,6 +1463,9 @@ __global__ void __launch_bounds__(256) gj_update_kernel(double* M, int n, int k0
 // (skipped after a zero pivot: the pivot list is then incomplete)
 __global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm,
                                      const int64_t* status) {
+  M += (int64_t)blockIdx.y * n * n;     // batched use: matrix blockIdx.y
+  perm += (int64_t)blockIdx.y * n;
+  status += blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || *status != 0) return;
   double* row = M + i * n;
@@ -1727,16 +1674,6 @@ __global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
-// ALEFSI_SPMV_V4 (A/B measurement only): 0 = 2x128-bit kernel, 1 = 256-bit
-// loads, unset/2 = 256-bit loads + shuffled block columns
-int spmv_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("ALEFSI_SPMV_V4");
-    return e == nullptr ? 2 : (e[0] == '0' ? 0 : e[0] == '1' ? 1 : 2);
-  }();
-  return v;
-}
-
 template <int NC>
 void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
                    cudaStream_t s) {
@@ -1754,12 +1691,10 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
   if constexpr (NC % 2 == 0) {
     const bool idx32 = A.nnzb * NC * NC < ((int64_t)1 << 31) && A.nnz_pp < ((int64_t)1 << 31) &&
                        A.n_nodes * NC < ((int64_t)1 << 31);
-    const int var = spmv_variant();
-    if (idx32 && NC == 4 && var > 0) {
-      const bool unr = A.n_nodes < kSmallLevelNodes && small_level_kernels_enabled();
-      auto k = var == 1 ? (mode == 0 ? spmv4_v4_kernel<0, false> : spmv4_v4_kernel<1, false>)
-               : unr    ? (mode == 0 ? spmv4_v4_kernel<0, true, true> : spmv4_v4_kernel<1, true, true>)
-                        : (mode == 0 ? spmv4_v4_kernel<0, true> : spmv4_v4_kernel<1, true>);
+    if (idx32 && NC == 4) {
+      const bool unr = A.n_nodes < kSmallLevelNodes;
+      auto k = unr ? (mode == 0 ? spmv4_kernel<0, true> : spmv4_kernel<1, true>)
+                   : (mode == 0 ? spmv4_kernel<0, false> : spmv4_kernel<1, false>);
       k<<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr, A.pp_indices,
                              A.pp_data, x, b, y);
       return;
@@ -1782,29 +1717,11 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
                                             A.pp_indices, A.pp_data, x, b, y);
 }
 
-// ALEFSI_APPLY_MERGE=0 launches every patch group separately (A/B only)
-bool apply_merge_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ALEFSI_APPLY_MERGE");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on;
-}
-
-// ALEFSI_APPLY_V4=0 keeps 16-byte column pieces (A/B measurement only)
-bool apply_v4_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ALEFSI_APPLY_V4");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on;
-}
-
 template <int NP, int LD, int NC>
 void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, cudaStream_t s) {
   bool v4 = false;
   if constexpr (LD % 4 == 0) {
-    v4 = apply_v4_enabled();
+    v4 = true;
     for (int i = 0; i < ng; ++i)
       v4 = v4 && reinterpret_cast<uintptr_t>(g[i].inv) % 32 == 0 &&
            reinterpret_cast<uintptr_t>(Y + g[i].y_offset) % 32 == 0;
@@ -1824,7 +1741,7 @@ void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, 
   }
   if (grid == 0) return;
   const int64_t total = G.n_patches[0] + G.n_patches[1];
-  if (total < kSmallPatchCount && small_level_kernels_enabled() && NP <= 108) {
+  if (total < kSmallPatchCount && NP <= 108) {
     // one CTA per patch, 4 column splits
     G.blocks0 = (int)G.n_patches[0];
     const int sgrid = (int)total;
@@ -1847,30 +1764,40 @@ void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, 
   vanka_apply_kernel<NP, LD, NC, 2><<<grid, ApplyShape<LD, 2>::BLK, 0, s>>>(G, d);
 }
 
-// batched global-memory Gauss-Jordan for large patches (see big_* kernels)
+// batched blocked Gauss-Jordan for the 500 x 500 macro patches (big_* and gj_*
+// kernels).  work: vanka_factorize_work(np, n_patches) doubles from the handle
+// (perm | src | rowslot | panel slabs | per-patch status), no allocation,
+// no synchronisation.
+constexpr int kBigKB = 16;
+
 void factorize_big(const DevMatrix& A, const DevPatchGroup& g, int64_t* status, cudaStream_t s) {
-  const int np_ = g.np;
-  const int64_t n = g.n_patches;
-  double *M = nullptr, *colk = nullptr, *prow = nullptr;
-  int *used = nullptr, *perm = nullptr;
-  cudaMalloc(&M, sizeof(double) * n * np_ * np_);
-  cudaMalloc(&colk, sizeof(double) * n * np_);
-  cudaMalloc(&prow, sizeof(double) * n * np_);
-  cudaMalloc(&used, sizeof(int) * n * np_);
-  cudaMalloc(&perm, sizeof(int) * n * np_);
-  const dim3 grid(64, (unsigned)n);
-  big_gather_kernel<<<grid, 256, 0, s>>>(A, np_, g.npn, g.nodes, M, used);
-  for (int k = 0; k < np_; ++k) {
-    big_pivot_kernel<<<(unsigned)n, 512, 0, s>>>(np_, k, M, used, perm, colk, prow, status);
-    big_eliminate_kernel<<<grid, 256, 0, s>>>(np_, k, M, perm, colk, prow);
+  const int n = g.np;
+  const int64_t P = g.n_patches;
+  double* M = g.inv;                                   // ld == np (checked by the caller)
+  int64_t* perm = reinterpret_cast<int64_t*>(g.work);
+  int* src = reinterpret_cast<int*>(perm + P * n);
+  int* rowslot = src + P * n;
+  double* slab = reinterpret_cast<double*>(rowslot + P * n);
+  int64_t* pstatus = reinterpret_cast<int64_t*>(slab + P * 2 * kBigKB * n);
+  static bool attr = [] {
+    cudaFuncSetAttribute(gj_panel_kernel<kBigKB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         225 * 1024);
+    return true;
+  }();
+  (void)attr;
+  cudaMemsetAsync(pstatus, 0, sizeof(int64_t) * P, s);
+  big_gather_kernel<<<dim3(32, (unsigned)P), 256, 0, s>>>(A, n, g.npn, g.nodes, M);
+  const size_t smem = (size_t)n * kBigKB * 8 + (size_t)n * 4;
+  const dim3 ug((unsigned)grid_for(n, 128), (unsigned)grid_for(n, 32), (unsigned)P);
+  for (int k0 = 0; k0 < n; k0 += kBigKB) {
+    const int kb = std::min(kBigKB, n - k0);
+    gj_panel_kernel<kBigKB><<<(unsigned)P, 512, smem, s>>>(M, n, k0, kb, perm, src, slab,
+                                                           rowslot, pstatus);
+    gj_update_kernel<kBigKB><<<ug, 256, 0, s>>>(M, n, k0, kb, src, slab, rowslot, pstatus);
   }
-  big_finalize_kernel<<<grid, 256, sizeof(int) * np_, s>>>(np_, g.ld, M, perm, g.inv);
-  cudaStreamSynchronize(s);
-  cudaFree(M);
-  cudaFree(colk);
-  cudaFree(prow);
-  cudaFree(used);
-  cudaFree(perm);
+  gj_unscramble_kernel<<<dim3((unsigned)grid_for(n, 128), (unsigned)P), 128, 0, s>>>(
+      M, n, perm, pstatus);
+  big_finish_kernel<<<dim3(32, (unsigned)P), 256, 0, s>>>(n, M, pstatus, status);
 }
 
 template <int NP, int NC, int W, int NPAT, int TAIL = 0>
@@ -1883,16 +1810,6 @@ void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* 
 
 constexpr int64_t kTailMinPatches = 8192;
 
-// ALEFSI_FACT_TAIL=0 (A/B only): the one-CTA-per-SM forms — all rows of the
-// 108 x 108 patches in registers, two 75 x 75 patches per CTA
-bool fact_tail_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ALEFSI_FACT_TAIL");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on;
-}
-
 }  // namespace
 
 void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
@@ -1901,6 +1818,12 @@ void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y
   if (A.nc == 4) spmv_dispatch<4>(A, x, b, y, mode, s);
   else if (A.nc == 3) spmv_dispatch<3>(A, x, b, y, mode, s);
   else if (A.nc == 2) spmv_dispatch<2>(A, x, b, y, mode, s);
+}
+
+int64_t vanka_factorize_work(int np, int64_t n_patches) {
+  if (np != 500) return 0;   // register kernels need no scratch
+  // perm (int64) + src, rowslot (int) + 2 KB slab rows + status, in doubles
+  return n_patches * ((int64_t)np * (2 + 2 * kBigKB) + 1);
 }
 
 bool vanka_supported(int nc, int np) {
@@ -1915,19 +1838,19 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
   else if (A.nc == 3 && g.np == 75) {
     // one patch per CTA (118 registers, two CTAs per SM) instead of two per
     // CTA (178 registers, one CTA): config 1 80 -> 70 ms, bitwise equal
-    if (fact_tail_enabled()) factorize_cw_dispatch<75, 3, 8, 1>(A, g, status, s);
-    else factorize_cw_dispatch<75, 3, 8, 2>(A, g, status, s);
+    factorize_cw_dispatch<75, 3, 8, 1>(A, g, status, s);
   }
   else if (A.nc == 4 && g.np == 108) {
     // two CTAs per SM; groups of >= 8192 patches (config 3: 134 -> 102 ms;
     // config 2, whose factorisation time is the coarse inverse's, unchanged)
-    if (fact_tail_enabled() && g.n_patches >= kTailMinPatches)
+    if (g.n_patches >= kTailMinPatches)
       factorize_cw_dispatch<108, 4, 12, 1, 12>(A, g, status, s);
     else factorize_cw_dispatch<108, 4, 12, 1>(A, g, status, s);
   }
   else if (A.nc == 2 && g.np == 18) factorize_cw_dispatch<18, 2, 2, 2>(A, g, status, s);
   else if (A.nc == 3 && g.np == 81) factorize_cw_dispatch<81, 3, 9, 2>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 500) factorize_big(A, g, status, s);
+  else if (A.nc == 4 && g.np == 500 && g.ld == g.np && g.work != nullptr)
+    factorize_big(A, g, status, s);
 }
 
 // one launch per pair of consecutive groups with the same patch size;
@@ -1937,8 +1860,7 @@ int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const 
   int launches = 0;
   for (int i = 0; i < n_groups;) {
     const DevPatchGroup& g = groups[i];
-    const int ng = (i + 1 < n_groups && groups[i + 1].np == g.np && groups[i + 1].ld == g.ld &&
-                    apply_merge_enabled())
+    const int ng = (i + 1 < n_groups && groups[i + 1].np == g.np && groups[i + 1].ld == g.ld)
                        ? 2 : 1;
     const DevPatchGroup* gp = groups + i;
     i += ng;
@@ -1955,15 +1877,6 @@ int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const 
   return launches;
 }
 
-// ALEFSI_GATHER4=0 keeps the thread-per-dof gather for NC = 4 (A/B only)
-bool gather4_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ALEFSI_GATHER4");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on;
-}
-
 void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int64_t* goff,
                          const double* weight, const double* Y, double* x, double omega,
                          int init_zero, cudaStream_t s) {
@@ -1971,7 +1884,7 @@ void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int
   if (ndof == 0) return;
   // large levels only: up to ~10^5 nodes a thread per dof (4x the threads)
   // is as fast or faster (140k nodes: 0.0114 vs 0.0121 ms)
-  if (nc == 4 && n_nodes >= 4 * kSmallLevelNodes && gather4_enabled() &&
+  if (nc == 4 && n_nodes >= 4 * kSmallLevelNodes &&
       reinterpret_cast<uintptr_t>(Y) % 32 == 0 &&
       reinterpret_cast<uintptr_t>(x) % 32 == 0) {
     vanka_gather4_kernel<<<grid_for(n_nodes, 256), 256, 0, s>>>(n_nodes, gptr, goff, weight, Y,
@@ -1982,30 +1895,12 @@ void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int
                                                            omega, init_zero);
 }
 
-// ALEFSI_SMALL_LEVELS=0 keeps the large-level kernels on every level (A/B only)
-bool small_level_kernels_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ALEFSI_SMALL_LEVELS");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on;
-}
-
-// ALEFSI_TRANSFER4=0 keeps the thread-per-dof transfer kernel (A/B only)
-bool transfer4_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ALEFSI_TRANSFER4");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on;
-}
-
 void launch_restrict(int64_t n_coarse, int nc, const int64_t* ptr, const int32_t* idx,
                      const double* val, const double* r_fine, const uint8_t* constrained_coarse,
                      double* b_coarse, cudaStream_t s) {
   // restriction rows are long (a coarse node collects ~100 fine nodes): a
   // thread per (row, component), or 8 lanes per (row, component) on small levels
-  if (n_coarse < kSmallLevelNodes && small_level_kernels_enabled())
+  if (n_coarse < kSmallLevelNodes)
     transfer_split_kernel<<<grid_for(n_coarse * nc * 8, 256), 256, 0, s>>>(
         n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
   else
@@ -2016,7 +1911,7 @@ void launch_restrict(int64_t n_coarse, int nc, const int64_t* ptr, const int32_t
 void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_t* idx,
                         const double* val, const double* x_coarse,
                         const uint8_t* constrained_fine, double* x_fine, cudaStream_t s) {
-  if (nc == 4 && vec4_ok(x_coarse, 0, 4) && vec4_ok(x_fine, 0, 4) && transfer4_enabled())
+  if (nc == 4 && vec4_ok(x_coarse, 0, 4) && vec4_ok(x_fine, 0, 4))
     transfer4_kernel<<<grid_for(n_fine, 128), 128, 0, s>>>(n_fine, ptr, idx, val, x_coarse,
                                                            constrained_fine, x_fine, 1);
   else
@@ -2031,22 +1926,11 @@ int gj_panel_width(int64_t n) {
   return 0;
 }
 
-// ALEFSI_GJ_BLOCKED=0 keeps the one-pivot-per-launch Gauss-Jordan (A/B only)
-bool gj_blocked_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("ALEFSI_GJ_BLOCKED");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on;
-}
-
-// ALEFSI_GJ_CLUSTER (A/B only): CTAs per cluster panel; 0 = single-CTA
-// panel kernel.  Default: 16 (non-portable size, 2d config 0 39.5 -> 37 ms vs
-// 8) where the device can co-schedule it, else 8, else the single-CTA panel
+// CTAs per cluster panel: 16 (non-portable size, 2d config 0 39.5 -> 37 ms
+// vs 8) where the device can co-schedule it, else 8, else 0 = the single-CTA
+// panel kernel
 int gj_cluster_size() {
   static const int c = [] {
-    const char* e = std::getenv("ALEFSI_GJ_CLUSTER");
-    if (e != nullptr) return std::atoi(e);
     cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
@@ -2077,20 +1961,11 @@ int gj_cluster_size() {
 }
 bool gj_cluster_enabled() { return gj_cluster_size() > 0; }
 
-// ALEFSI_GJ_KB=32 (A/B only): 32-column cluster panels — half the update
-// passes, but slower overall (config 2 18.2 -> 18.9 ms, config 1 50.3 -> 51.6)
-int gj_cluster_kb() {
-  static const int v = [] {
-    const char* e = std::getenv("ALEFSI_GJ_KB");
-    return e != nullptr && std::atoi(e) == 32 ? 32 : 16;
-  }();
-  return v;
-}
-
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s) {
   // cluster panels: the n x 16 panel spread over 8-16 SMs fits for every n <= kGjMaxN
-  const bool clus = gj_blocked_enabled() && gj_cluster_enabled() && n >= 128;
-  const int nb = clus ? gj_cluster_kb() : gj_blocked_enabled() ? gj_panel_width(n) : 0;
+  // (32-column cluster panels measured slower: config 2 18.2 -> 18.9 ms)
+  const bool clus = gj_cluster_enabled() && n >= 128;
+  const int nb = clus ? 16 : gj_panel_width(n);
   if (nb > 0 && n <= kGjMaxN) {
     // work: perm (n int64) | src (n int) | rowslot (n int) | slab (2 nb x n)
     int64_t* perm = reinterpret_cast<int64_t*>(work);
@@ -2119,10 +1994,6 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
       cudaFuncSetAttribute(gj_panel_cluster_kernel<16>,
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(gj_panel_cluster_kernel<32>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
-      cudaFuncSetAttribute(gj_panel_cluster_kernel<32>,
-                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       return true;
     }();
     (void)cattr;
@@ -2140,10 +2011,7 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
     cfg.numAttrs = 1;
     for (int64_t k0 = 0; k0 < n; k0 += nb) {
       const int kb = (int)std::min<int64_t>(nb, n - k0);
-      if (clus && nb == 32)
-        cudaLaunchKernelEx(&cfg, gj_panel_cluster_kernel<32>, M, (int)n, (int)k0, kb, R, perm, src,
-                           slab, rowslot, status);
-      else if (clus)
+      if (clus)
         cudaLaunchKernelEx(&cfg, gj_panel_cluster_kernel<16>, M, (int)n, (int)k0, kb, R, perm, src,
                            slab, rowslot, status);
       else if (nb == 16)
@@ -2155,11 +2023,7 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
       else
         gj_panel_kernel<4><<<1, 512, smem, s>>>(M, (int)n, (int)k0, kb, perm, src, slab,
                                                 rowslot, status);
-      if (nb == 32)
-        gj_update_kernel<32><<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot,
-                                                status);
-      else
-        gj_update_kernel<16><<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot,
+      gj_update_kernel<16><<<ug, 256, 0, s>>>(M, (int)n, (int)k0, kb, src, slab, rowslot,
                                                 status);
     }
     gj_unscramble_kernel<<<grid_for(n, 128), 128, 0, s>>>(M, n, perm, status);

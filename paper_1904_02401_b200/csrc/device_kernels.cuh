@@ -30,10 +30,13 @@ struct DevPatchGroup {
   const int32_t* nodes = nullptr;   // (n_patches, npn)
   double* inv = nullptr;            // (n_patches, np, ld) column-major inverses
   int64_t y_offset = 0;             // start of this group's rows in Y
+  double* work = nullptr;           // factorisation scratch, vanka_factorize_work doubles
 };
 
 // (nc, dofs per patch) combinations with compiled Vanka kernels
 bool vanka_supported(int nc, int np);
+// factorisation scratch of a patch group in doubles (0: none needed)
+int64_t vanka_factorize_work(int np, int64_t n_patches);
 // gather A_i = R_i A R_i^T and invert (Gauss-Jordan, partial pivoting);
 // singular patches set *status to 1 + patch index (first one wins)
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,

@@ -111,6 +111,7 @@ struct Group {
   int64_t n_patches = 0, y_offset = 0;
   DevBuf<int32_t> nodes;
   DevBuf<double> inv;
+  DevBuf<double> fwork;   // factorisation scratch (500 x 500 macro patches), kept
 };
 
 struct Level {
@@ -460,7 +461,10 @@ struct MgHandle {
       int64_t off = 0;
       for (auto& g : L.groups) {
         CK(g->inv.ensure((size_t)g->n_patches * g->np * g->ld));
+        const int64_t wn = vanka_factorize_work(g->np, g->n_patches);
+        if (wn > 0) CK(g->fwork.ensure((size_t)wn));
         DevPatchGroup dg;
+        dg.work = g->fwork.p;
         dg.npn = g->npn;
         dg.np = g->np;
         dg.ld = g->ld;
@@ -803,6 +807,9 @@ int alefsi_mg_asm_setup(alefsi_mg h, int32_t level, int32_t dim, int64_t n_cells
   auto& L = m->lv[level];
   if (!L.has_matrix) return fail(ALEFSI_ERR_STATE, "set_pattern before asm_setup");
   if (dim + 1 != m->nc || (dim != 2 && dim != 3)) return fail(ALEFSI_ERR_ARG, "asm: bad dim");
+  // the cell kernels keep block slots as 32-bit ints in shared memory
+  if (L.nnzb >= ((int64_t)1 << 31))
+    return fail(ALEFSI_ERR_ARG, "asm: device assembly needs fewer than 2^31 blocks per level");
   const int nb = dim == 3 ? 27 : 9;
   L.dim = dim;
   CKAPI(L.asm_cell_nodes.upload(cell_nodes, (size_t)n_cells * nb, m->stream));
@@ -830,10 +837,14 @@ int alefsi_mg_asm_tables(alefsi_mg h, int32_t dim, int32_t nq, const double* N, 
   MgHandle* m = H(h);
   if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
   const int nb = dim == 3 ? 27 : 9;
-  if (nq > 27) return fail(ALEFSI_ERR_ARG, "asm: at most 27 quadrature points");
-  cudaStreamSynchronize(m->stream);
-  alefsi::set_assembly_tables(N, dN, w, nq, nb, dim);
-  CKAPI(cudaGetLastError());
+  if (dim != 2 && dim != 3) return fail(ALEFSI_ERR_ARG, "asm: dim must be 2 or 3");
+  if (nq != nb)
+    return fail(ALEFSI_ERR_ARG, "asm: the Q2 kernels integrate with nq == nb quadrature points");
+  const int rc = alefsi::set_assembly_tables(N, dN, w, nq, nb, dim);
+  if (rc == 2)
+    return fail(ALEFSI_ERR_ARG, "asm: shape tables differ from those already loaded for dim " +
+                                    std::to_string(dim));
+  if (rc != 0) return fail(ALEFSI_ERR_CUDA, "asm: loading the shape tables failed");
   return ALEFSI_OK;
 }
 
