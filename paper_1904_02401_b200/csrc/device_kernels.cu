@@ -316,6 +316,75 @@ __global__ void __launch_bounds__(256) spmv_half_kernel(int64_t n, const int64_t
   }
 }
 
+// 2D (NC = 3) operator in sliced-ELL form: warp = 32 consecutive block rows,
+// lane = row.  Every element of a slot is one coalesced 256-byte warp load
+// (evict-first), the column index one 128-byte load; the x block is read
+// through the read-only path (x stays L2-resident).  A row sums its blocks
+// in pattern order, then its pressure-extension entries.  Padding slots hold
+// zeros and a valid column.
+template <int MODE>
+__global__ void __launch_bounds__(256) spmv3_sell_kernel(int64_t n, int64_t n_slices,
+                                                         const int64_t* __restrict__ off,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const int64_t* __restrict__ poff,
+                                                         const int32_t* __restrict__ pcol,
+                                                         const double* __restrict__ pval,
+                                                         const double* __restrict__ x,
+                                                         const double* __restrict__ b,
+                                                         double* __restrict__ y) {
+  constexpr int NC = 3;
+  const int lane = threadIdx.x & 31;
+  const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (sl >= n_slices) return;
+  const int64_t row = sl * 32 + lane;
+  const int64_t g0 = off[sl], g1 = off[sl + 1];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 2
+  for (int64_t g = g0; g < g1; ++g) {
+    const int c = __ldcs(col + g * 32 + lane);
+    const double* v = val + g * (NC * NC * 32) + lane;
+    double e[NC * NC];
+#pragma unroll
+    for (int q = 0; q < NC * NC; ++q) e[q] = __ldcs(v + q * 32);
+    const double x0 = __ldg(x + (int64_t)c * NC), x1 = __ldg(x + (int64_t)c * NC + 1),
+                 x2 = __ldg(x + (int64_t)c * NC + 2);
+    a0 = fma(e[0], x0, a0); a0 = fma(e[1], x1, a0); a0 = fma(e[2], x2, a0);
+    a1 = fma(e[3], x0, a1); a1 = fma(e[4], x1, a1); a1 = fma(e[5], x2, a1);
+    a2 = fma(e[6], x0, a2); a2 = fma(e[7], x1, a2); a2 = fma(e[8], x2, a2);
+  }
+  if (poff != nullptr) {
+    double ap = 0.0;
+    const int64_t p0 = poff[sl], p1 = poff[sl + 1];
+#pragma unroll 4
+    for (int64_t g = p0; g < p1; ++g)
+      ap = fma(__ldcs(pval + g * 32 + lane), __ldg(x + (int64_t)__ldcs(pcol + g * 32 + lane) * NC), ap);
+    a0 += ap;
+  }
+  if (row >= n) return;
+  const int64_t o = row * NC;
+  if (MODE == 1) {
+    y[o] = b[o] - a0;
+    y[o + 1] = b[o + 1] - a1;
+    y[o + 2] = b[o + 2] - a2;
+  } else {
+    y[o] = a0;
+    y[o + 1] = a1;
+    y[o + 2] = a2;
+  }
+}
+
+__global__ void sell_pack_kernel(int64_t n_pos, int nc2, const int64_t* __restrict__ map,
+                                 const double* __restrict__ data, double* __restrict__ val) {
+  for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < n_pos;
+       pos += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = map[pos];
+    const int64_t g = pos >> 5, lane = pos & 31;
+    double* out = val + g * nc2 * 32 + lane;
+    for (int q = 0; q < nc2; ++q) out[q * 32] = m >= 0 ? data[m * nc2 + q] : 0.0;
+  }
+}
+
 // --------------------------------------------------------------------------
 // Vanka apply: Y[p] = A_p^{-1} d[dofs_p].  Inverses are stored column-major
 // with an even column length LD, so thread t of a patch owns rows
@@ -1503,12 +1572,14 @@ constexpr int kBatch = 8;
 // into the first pass.  VW = 1: scalar path for lengths that are not a
 // multiple of 4 (2D).  Fixed element-to-thread map: deterministic.
 template <int VW>
-__global__ void __launch_bounds__(256) multi_dot_kernel(int nvec, const double* __restrict__ V,
+__global__ void __launch_bounds__(256) multi_dot_kernel(const GmresCtl* __restrict__ ctl,
+                                                        const double* __restrict__ V,
                                                         int64_t ldv, const double* __restrict__ w,
                                                         int64_t n, double* __restrict__ partial,
                                                         const int* flag) {
   if (flag != nullptr && *flag == 0) return;
   __shared__ double red[8];
+  const int nvec = ctl->k + 1;            // basis vectors v_0 .. v_k
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
   const int nout = nvec + 1;
@@ -1555,13 +1626,18 @@ __global__ void __launch_bounds__(256) multi_dot_kernel(int nvec, const double* 
   if (threadIdx.x == 0) partial[(int64_t)blockIdx.x * nout + nvec] = s;
 }
 
+// out[j] = sum of the blocks' partials j, one CTA per output; nout = k + 2
+// (multi_dot) when ctl is given, else the fixed count
 __global__ void __launch_bounds__(256) reduce_partials_kernel(int nout, int nblocks,
                                                               const double* __restrict__ partial,
                                                               double* __restrict__ out,
-                                                              const int* flag) {
+                                                              const int* flag,
+                                                              const GmresCtl* ctl) {
   if (flag != nullptr && *flag == 0) return;
-  __shared__ double red[8];
+  if (ctl != nullptr) nout = ctl->k + 2;
   const int j = blockIdx.x;
+  if (j >= nout) return;
+  __shared__ double red[8];
   double acc = 0.0;
   for (int b = threadIdx.x; b < nblocks; b += blockDim.x) acc += partial[(int64_t)b * nout + j];
   const double s = block_sum_256(acc, red);
@@ -1569,7 +1645,8 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(int nout, int nblo
 }
 
 template <int VW>
-__global__ void __launch_bounds__(256) multi_axpy_kernel(int nvec, const double* __restrict__ V,
+__global__ void __launch_bounds__(256) multi_axpy_kernel(const GmresCtl* __restrict__ ctl,
+                                                         const double* __restrict__ V,
                                                          int64_t ldv, const double* __restrict__ h,
                                                          double* __restrict__ w, int64_t n,
                                                          double* __restrict__ partial,
@@ -1577,6 +1654,7 @@ __global__ void __launch_bounds__(256) multi_axpy_kernel(int nvec, const double*
   if (flag != nullptr && *flag == 0) return;
   __shared__ double hs[512];
   __shared__ double red[8];
+  const int nvec = ctl->k + 1;
   for (int j = threadIdx.x; j < nvec; j += blockDim.x) hs[j] = h[j];
   __syncthreads();
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1620,39 +1698,119 @@ __global__ void __launch_bounds__(256) multi_axpy_kernel(int nvec, const double*
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
 
-// stage 0: decide re-orthogonalisation (Kahan test of linsolve.py:79-83);
+// stage 0: decide re-orthogonalisation (Kahan test of linsolve.py:79-83,
+// ||w|| after the first pass vs hcol[k+1] = ||w||^2 before it);
 // stage 1: fold the second projection into the Hessenberg column and set
 // H[k+1, k] = ||w||.
-__global__ void arnoldi_finish_kernel(int k, double* hcol, const double* h2, const double* nb2,
-                                      const double* na2, int* flag, int stage) {
+__global__ void arnoldi_finish_kernel(GmresCtl* ctl, double* hcol, const double* h2,
+                                      const double* na2, int stage) {
+  const int k = ctl->k;
   if (stage == 0) {
-    if (threadIdx.x == 0) *flag = (sqrt(*na2) < 0.7071 * sqrt(*nb2)) ? 1 : 0;
+    if (threadIdx.x == 0) ctl->flag = (sqrt(*na2) < 0.7071 * sqrt(hcol[k + 1])) ? 1 : 0;
     return;
   }
-  if (*flag)
+  if (ctl->flag)
     for (int j = threadIdx.x; j <= k; j += blockDim.x) hcol[j] += h2[j];
+  __syncthreads();
   if (threadIdx.x == 0) hcol[k + 1] = sqrt(*na2);
 }
 
-__global__ void scale_copy_kernel(const double* __restrict__ w, double* __restrict__ v,
-                                  const double* hkk1, int64_t n) {
-  const double h = *hkk1;
+// v_{k+1} = w / H[k+1, k] (linsolve.py:85-86), also into the V-cycle's input
+// buffer for the next Arnoldi step
+__global__ void scale_copy_slot_kernel(const GmresCtl* __restrict__ ctl,
+                                       const double* __restrict__ w, double* __restrict__ V,
+                                       int64_t ldv, const double* __restrict__ hcol,
+                                       double* __restrict__ vin, int64_t n) {
+  const int k = ctl->k;
+  const double h = hcol[k + 1];
   if (!(h > 0.0)) return;
+  double* v = V + (int64_t)(k + 1) * ldv;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    v[i] = w[i] / h;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = w[i] / h;
+    v[i] = t;
+    vin[i] = t;
+  }
 }
 
-__global__ void div_kernel(const double* __restrict__ x, double* __restrict__ y, double a,
-                           int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = x[i] / a;
+// beta = ||b||, tolerance, early exit (linsolve.py:55-60); v_0 = b / beta
+__global__ void gmres_init_kernel(GmresCtl* ctl, const double* bb, double* res, double* g,
+                                  cudaGraphConditionalHandle cond, int use_cond) {
+  const double beta = sqrt(*bb);
+  const double tol = fmax(ctl->rel_tol * beta, ctl->abs_tol);
+  const int stop = (beta == 0.0 || beta <= tol) ? 1 : 0;
+  ctl->beta = beta;
+  ctl->tol = tol;
+  ctl->k = 0;
+  ctl->its = 0;
+  ctl->done = stop;
+  ctl->converged = 1;
+  res[0] = beta;
+  g[0] = beta;
+  if (use_cond) cudaGraphSetConditional(cond, stop ? 0u : 1u);
 }
 
-__global__ void combine_kernel(int nvec, const double* __restrict__ V, int64_t ldv,
-                               const double* __restrict__ c, double* __restrict__ y, int64_t n) {
+__global__ void scale_dual_kernel(const GmresCtl* __restrict__ ctl, const double* __restrict__ b,
+                                  double* __restrict__ v0, double* __restrict__ vin, int64_t n) {
+  if (ctl->done) return;
+  const double beta = ctl->beta;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double t = b[i] / beta;
+    v0[i] = t;
+    vin[i] = t;
+  }
+}
+
+// Hessenberg column k, accumulated Givens rotations and the new one, the
+// residual estimate |g[k+1]| and the stopping test (linsolve.py:88-102);
+// H is (hstride + 1) x hstride row-major.  Sets the while-node condition.
+__global__ void givens_kernel(GmresCtl* ctl, const double* __restrict__ hcol, double* H,
+                              double* cs, double* sn, double* g, double* res,
+                              cudaGraphConditionalHandle cond, int use_cond) {
+  const int k = ctl->k, m = ctl->hstride;
+  auto Hat = [&](int i, int j) -> double& { return H[(int64_t)i * m + j]; };
+  for (int i = 0; i <= k + 1; ++i) Hat(i, k) = hcol[i];
+  for (int i = 0; i < k; ++i) {
+    const double t = cs[i] * Hat(i, k) + sn[i] * Hat(i + 1, k);
+    Hat(i + 1, k) = -sn[i] * Hat(i, k) + cs[i] * Hat(i + 1, k);
+    Hat(i, k) = t;
+  }
+  const double r = hypot(Hat(k, k), Hat(k + 1, k));
+  cs[k] = Hat(k, k) / r;
+  sn[k] = Hat(k + 1, k) / r;
+  Hat(k, k) = r;
+  Hat(k + 1, k) = 0.0;
+  g[k + 1] = -sn[k] * g[k];
+  g[k] = cs[k] * g[k];
+  const double rr = fabs(g[k + 1]);
+  res[k + 1] = rr;
+  const int conv = rr <= ctl->tol ? 1 : 0;
+  const int stop = conv || k + 1 >= ctl->max_iter;
+  ctl->its = k + 1;
+  ctl->converged = conv;
+  ctl->done = stop;
+  ctl->k = k + 1;
+  if (use_cond) cudaGraphSetConditional(cond, stop ? 0u : 1u);
+}
+
+// y = triu(H)^{-1} g (linsolve.py:107), column-oriented back substitution
+__global__ void backsolve_kernel(const GmresCtl* ctl, const double* H, const double* g,
+                                 double* y) {
+  const int its = ctl->its, m = ctl->hstride;
+  for (int j = 0; j < its; ++j) y[j] = g[j];
+  for (int j = its - 1; j >= 0; --j) {
+    y[j] /= H[(int64_t)j * m + j];
+    for (int i = 0; i < j; ++i) y[i] -= y[j] * H[(int64_t)i * m + j];
+  }
+}
+
+// out = sum_j c[j] V[j] over the its basis vectors (V y of linsolve.py:108)
+__global__ void combine_kernel(const GmresCtl* __restrict__ ctl, const double* __restrict__ V,
+                               int64_t ldv, const double* __restrict__ c, double* __restrict__ y,
+                               int64_t n) {
   __shared__ double cs[512];
+  const int nvec = ctl->its;
   for (int j = threadIdx.x; j < nvec; j += blockDim.x) cs[j] = c[j];
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1679,6 +1837,18 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
                    cudaStream_t s) {
   const int grid = grid_for(A.n_nodes * 32, 256);
   if constexpr (NC == 3) {
+    if (A.sell_off != nullptr) {
+      const int sgrid = grid_for(A.n_slices * 32, 256);
+      if (mode == 0)
+        spmv3_sell_kernel<0><<<sgrid, 256, 0, s>>>(A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
+                                                   A.sell_val, A.sell_poff, A.sell_pcol,
+                                                   A.sell_pval, x, b, y);
+      else
+        spmv3_sell_kernel<1><<<sgrid, 256, 0, s>>>(A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
+                                                   A.sell_val, A.sell_poff, A.sell_pcol,
+                                                   A.sell_pval, x, b, y);
+      return;
+    }
     const int hgrid = grid_for(A.n_nodes * 16, 256);
     if (mode == 0)
       spmv_half_kernel<NC, 0><<<hgrid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
@@ -1818,6 +1988,13 @@ void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y
   if (A.nc == 4) spmv_dispatch<4>(A, x, b, y, mode, s);
   else if (A.nc == 3) spmv_dispatch<3>(A, x, b, y, mode, s);
   else if (A.nc == 2) spmv_dispatch<2>(A, x, b, y, mode, s);
+}
+
+void launch_sell_pack(int64_t n_pos, int nc2, const int64_t* map, const double* data, double* val,
+                      cudaStream_t s) {
+  if (n_pos == 0) return;
+  sell_pack_kernel<<<(int)std::min<int64_t>(grid_for(n_pos, 256), 4 * 148 * 8), 256, 0, s>>>(
+      n_pos, nc2, map, data, val);
 }
 
 int64_t vanka_factorize_work(int np, int64_t n_patches) {
@@ -2049,47 +2226,59 @@ void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
   dense_matvec_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, M, x, y);
 }
 
-void launch_multi_dot(int nvec, const double* V, int64_t ldv, const double* w, int64_t n,
-                      double* partial, double* out, const int* flag, cudaStream_t s) {
+int launch_multi_dot(GmresCtl* ctl, int max_nvec, const double* V, int64_t ldv, const double* w,
+                     int64_t n, double* partial, double* out, const int* flag, cudaStream_t s) {
   if (vec4_ok(V, ldv, n) && vec4_ok(w, 0, n))
-    multi_dot_kernel<4><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, w, n, partial, flag);
+    multi_dot_kernel<4><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, w, n, partial, flag);
   else
-    multi_dot_kernel<1><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, w, n, partial, flag);
-  reduce_partials_kernel<<<nvec + 1, 256, 0, s>>>(nvec + 1, kRedBlocks, partial, out, flag);
+    multi_dot_kernel<1><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, w, n, partial, flag);
+  reduce_partials_kernel<<<max_nvec + 1, 256, 0, s>>>(0, kRedBlocks, partial, out, flag, ctl);
+  return 2;
 }
 
-void launch_multi_axpy(int nvec, const double* V, int64_t ldv, const double* h, double* w,
-                       int64_t n, double* partial, double* out, const int* flag,
-                       cudaStream_t s) {
+int launch_multi_axpy(GmresCtl* ctl, const double* V, int64_t ldv, const double* h, double* w,
+                      int64_t n, double* partial, double* out, const int* flag, cudaStream_t s) {
   if (vec4_ok(V, ldv, n) && vec4_ok(w, 0, n))
-    multi_axpy_kernel<4><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, h, w, n, partial, flag);
+    multi_axpy_kernel<4><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, h, w, n, partial, flag);
   else
-    multi_axpy_kernel<1><<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, h, w, n, partial, flag);
-  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, out, flag);
+    multi_axpy_kernel<1><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, h, w, n, partial, flag);
+  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, out, flag, nullptr);
+  return 2;
 }
 
-void launch_arnoldi_finish(int k, double* hcol, double* h2, const double* nb2, double* na2,
-                           int* flag, int stage, cudaStream_t s) {
-  arnoldi_finish_kernel<<<1, 256, 0, s>>>(k, hcol, h2, nb2, na2, flag, stage);
+int launch_arnoldi_finish(GmresCtl* ctl, double* hcol, double* h2, const double* na2, int stage,
+                          cudaStream_t s) {
+  arnoldi_finish_kernel<<<1, 256, 0, s>>>(ctl, hcol, h2, na2, stage);
+  return 1;
 }
 
-void launch_scale_copy(const double* w, double* v, const double* hkk1, int64_t n,
-                       cudaStream_t s) {
-  scale_copy_kernel<<<kRedBlocks, 256, 0, s>>>(w, v, hkk1, n);
+int launch_scale_copy_slot(const GmresCtl* ctl, const double* w, double* V, int64_t ldv,
+                           const double* hcol, double* vin, int64_t n, cudaStream_t s) {
+  scale_copy_slot_kernel<<<kRedBlocks, 256, 0, s>>>(ctl, w, V, ldv, hcol, vin, n);
+  return 1;
 }
 
-void launch_scale(const double* x, double* y, double alpha, int64_t n, cudaStream_t s) {
-  div_kernel<<<kRedBlocks, 256, 0, s>>>(x, y, alpha, n);
+int launch_gmres_init(GmresCtl* ctl, const double* b, int64_t n, double* partial, double* scal,
+                      double* res, double* g, double* v0, double* vin,
+                      cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
+  sumsq_kernel<<<kRedBlocks, 256, 0, s>>>(b, n, partial);
+  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, scal, nullptr, nullptr);
+  gmres_init_kernel<<<1, 1, 0, s>>>(ctl, scal, res, g, cond, use_cond);
+  scale_dual_kernel<<<kRedBlocks, 256, 0, s>>>(ctl, b, v0, vin, n);
+  return 4;
 }
 
-void launch_combine(int nvec, const double* V, int64_t ldv, const double* c, double* y,
-                    int64_t n, cudaStream_t s) {
-  combine_kernel<<<kRedBlocks, 256, 0, s>>>(nvec, V, ldv, c, y, n);
+int launch_givens(GmresCtl* ctl, const double* hcol, double* H, double* cs, double* sn, double* g,
+                  double* res, cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
+  givens_kernel<<<1, 1, 0, s>>>(ctl, hcol, H, cs, sn, g, res, cond, use_cond);
+  return 1;
 }
 
-void launch_sumsq(const double* x, int64_t n, double* partial, double* out, cudaStream_t s) {
-  sumsq_kernel<<<kRedBlocks, 256, 0, s>>>(x, n, partial);
-  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, out, nullptr);
+int launch_gmres_solution(const GmresCtl* ctl, const double* H, const double* g, double* y,
+                          const double* V, int64_t ldv, double* out, int64_t n, cudaStream_t s) {
+  backsolve_kernel<<<1, 1, 0, s>>>(ctl, H, g, y);
+  combine_kernel<<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, y, out, n);
+  return 2;
 }
 
 }  // namespace alefsi

@@ -15,7 +15,22 @@ struct DevMatrix {
   const int64_t* pp_indptr = nullptr;
   const int32_t* pp_indices = nullptr;
   const double* pp_data = nullptr;
+  // optional sliced-ELL copy used by the SpMV (nc == 3): slices of 32
+  // consecutive block rows, slice s holds its rows' k-th blocks in slot
+  // off[s] + k, a slot = nc*nc element planes of 32 doubles (one per row)
+  int64_t n_slices = 0;
+  const int64_t* sell_off = nullptr;    // n_slices + 1 (slot units)
+  const int32_t* sell_col = nullptr;    // slots * 32 block columns
+  const double* sell_val = nullptr;     // slots * nc*nc * 32
+  const int64_t* sell_poff = nullptr;   // pressure extension, same scheme (nullptr: none)
+  const int32_t* sell_pcol = nullptr;
+  const double* sell_pval = nullptr;
 };
+
+// refresh the sliced-ELL values from the CSR data: map[pos] = CSR block (or
+// entry) index of slot position pos, -1 for padding (stored as zero)
+void launch_sell_pack(int64_t n_pos, int nc2, const int64_t* map, const double* data, double* val,
+                      cudaStream_t s);
 
 // y = A x (mode 0) or y = b - A x (mode 1)
 void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
@@ -65,25 +80,42 @@ inline int64_t dense_inverse_work(int64_t n) { return 2 * n + 2 + 64 * n; }
 void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
                          cudaStream_t s);
 
-// ---- Krylov vector kernels (deterministic fixed-order reductions)
+// ---- GMRES (reference linsolve.py:41-115) with its state on the device, so
+// that a whole solve can run as one CUDA graph (conditional while node).
+// Every launcher returns the number of kernels it enqueued.
+struct GmresCtl {
+  int k;            // current Arnoldi step (0-based)
+  int its;          // completed iterations
+  int done;         // stop (converged or max_iter)
+  int converged;
+  int flag;         // second Gram-Schmidt pass needed (Kahan test)
+  int max_iter;
+  int hstride;      // Hessenberg row length (workspace capacity)
+  int pad;
+  double beta, tol, rel_tol, abs_tol;
+};
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs
-// out[j] = sum_i V[j*ldv + i] * w[i] for j < nvec; out[nvec] = sum_i w[i]^2
-// flag (optional): skip unless *flag != 0
-void launch_multi_dot(int nvec, const double* V, int64_t ldv, const double* w, int64_t n,
-                      double* partial, double* out, const int* flag, cudaStream_t s);
-// w[i] -= sum_j h[j] V[j*ldv + i]; out[0] = sum_i w[i]^2 (after update)
-void launch_multi_axpy(int nvec, const double* V, int64_t ldv, const double* h, double* w,
-                       int64_t n, double* partial, double* out, const int* flag,
-                       cudaStream_t s);
-// Arnoldi bookkeeping on device (see mg.cu)
-void launch_arnoldi_finish(int k, double* hcol, double* h2, const double* nb2, double* na2,
-                           int* flag, int stage, cudaStream_t s);
-void launch_scale_copy(const double* w, double* v, const double* hkk1, int64_t n,
-                       cudaStream_t s);
-void launch_scale(const double* x, double* y, double alpha, int64_t n, cudaStream_t s);
-// y = sum_j c[j] V[j*ldv + i]  (c on device)
-void launch_combine(int nvec, const double* V, int64_t ldv, const double* c, double* y,
-                    int64_t n, cudaStream_t s);
-void launch_sumsq(const double* x, int64_t n, double* partial, double* out, cudaStream_t s);
+// hcol[j] = v_j . w (j <= k), hcol[k+1] = w . w; deterministic two-stage sums;
+// flag (optional): skip unless *flag != 0; max_nvec bounds k + 1
+int launch_multi_dot(GmresCtl* ctl, int max_nvec, const double* V, int64_t ldv, const double* w,
+                     int64_t n, double* partial, double* out, const int* flag, cudaStream_t s);
+// w -= sum_{j<=k} h[j] v_j; out[0] = w . w (after)
+int launch_multi_axpy(GmresCtl* ctl, const double* V, int64_t ldv, const double* h, double* w,
+                      int64_t n, double* partial, double* out, const int* flag, cudaStream_t s);
+int launch_arnoldi_finish(GmresCtl* ctl, double* hcol, double* h2, const double* na2, int stage,
+                          cudaStream_t s);
+// v_{k+1} = w / hcol[k+1] into V and into the V-cycle input buffer vin
+int launch_scale_copy_slot(const GmresCtl* ctl, const double* w, double* V, int64_t ldv,
+                           const double* hcol, double* vin, int64_t n, cudaStream_t s);
+// beta, tol, early exit, v_0 = b / beta (into V and vin); sets the condition
+int launch_gmres_init(GmresCtl* ctl, const double* b, int64_t n, double* partial, double* scal,
+                      double* res, double* g, double* v0, double* vin,
+                      cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s);
+// Givens update of column k, residual estimate, stopping test; k += 1
+int launch_givens(GmresCtl* ctl, const double* hcol, double* H, double* cs, double* sn, double* g,
+                  double* res, cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s);
+// out = V triu(H)^{-1} g over the completed iterations
+int launch_gmres_solution(const GmresCtl* ctl, const double* H, const double* g, double* y,
+                          const double* V, int64_t ldv, double* out, int64_t n, cudaStream_t s);
 
 }  // namespace alefsi

@@ -159,6 +159,13 @@ struct Level {
   DevBuf<double> lps_val;
   DevBuf<uint8_t> dir_mask;
 
+  // sliced-ELL copy of the operator for the SpMV (nc == 3), see DevMatrix
+  int64_t n_slices = 0, sell_slots = 0, sell_pslots = 0;
+  bool sell_dirty = false;
+  DevBuf<int64_t> sell_off, sell_poff, sell_map, sell_pmap;
+  DevBuf<int32_t> sell_col, sell_pcol;
+  DevBuf<double> sell_val, sell_pval;
+
   int64_t ndof() const { return n_nodes * nc; }
   DevMatrix mat() const {
     DevMatrix m;
@@ -172,9 +179,86 @@ struct Level {
     m.pp_indptr = nnz_pp > 0 ? pp_indptr.p : nullptr;
     m.pp_indices = pp_indices.p;
     m.pp_data = pp_data.p;
+    if (n_slices > 0) {
+      m.n_slices = n_slices;
+      m.sell_off = sell_off.p;
+      m.sell_col = sell_col.p;
+      m.sell_val = sell_val.p;
+      if (sell_pslots > 0) {
+        m.sell_poff = sell_poff.p;
+        m.sell_pcol = sell_pcol.p;
+        m.sell_pval = sell_pval.p;
+      }
+    }
     return m;
   }
 };
+
+// Sliced-ELL index of a CSR pattern (32-row slices, no row permutation: the
+// Q2 node numbering keeps rows of one slice at nearly equal length — config 1
+// finest level: 0.25 % block padding).  pos = slot * 32 + lane.
+void sell_index(int64_t n, const int64_t* ptr, const int32_t* idx, std::vector<int64_t>& off,
+                std::vector<int32_t>& col, std::vector<int64_t>& map) {
+  const int64_t ns = (n + 31) / 32;
+  off.assign(ns + 1, 0);
+  for (int64_t sl = 0; sl < ns; ++sl) {
+    int64_t w = 0;
+    for (int64_t r = sl * 32; r < std::min(n, sl * 32 + 32); ++r) w = std::max(w, ptr[r + 1] - ptr[r]);
+    off[sl + 1] = off[sl] + w;
+  }
+  col.assign((size_t)off[ns] * 32, 0);
+  map.assign((size_t)off[ns] * 32, -1);
+  for (int64_t sl = 0; sl < ns; ++sl)
+    for (int lane = 0; lane < 32; ++lane) {
+      const int64_t r = sl * 32 + lane;
+      const int64_t len = r < n ? ptr[r + 1] - ptr[r] : 0;
+      for (int64_t k = 0; k < off[sl + 1] - off[sl]; ++k) {
+        const size_t pos = (size_t)(off[sl] + k) * 32 + lane;
+        // padding: zero value on a valid column (the row itself, else 0)
+        col[pos] = k < len ? idx[ptr[r] + k] : (int32_t)(r < n ? r : 0);
+        map[pos] = k < len ? ptr[r] + k : -1;
+      }
+    }
+}
+
+int build_sell(Level& L, const int64_t* indptr, const int32_t* indices, const int64_t* pp_indptr,
+               const int32_t* pp_indices, cudaStream_t s) {
+  L.n_slices = 0;
+  L.sell_slots = L.sell_pslots = 0;
+  if (L.nc != 3 || L.n_nodes == 0) return ALEFSI_OK;
+  std::vector<int64_t> off, map;
+  std::vector<int32_t> col;
+  sell_index(L.n_nodes, indptr, indices, off, col, map);
+  const int64_t ns = (int64_t)off.size() - 1;
+  CK(L.sell_off.upload(off.data(), off.size(), s));
+  CK(L.sell_col.upload(col.data(), col.size(), s));
+  CK(L.sell_map.upload(map.data(), map.size(), s));
+  CK(L.sell_val.ensure((size_t)off[ns] * 32 * 9));
+  L.sell_slots = off[ns];
+  if (L.nnz_pp > 0) {
+    std::vector<int64_t> poff, pmap;
+    std::vector<int32_t> pcol;
+    sell_index(L.n_nodes, pp_indptr, pp_indices, poff, pcol, pmap);
+    CK(L.sell_poff.upload(poff.data(), poff.size(), s));
+    CK(L.sell_pcol.upload(pcol.data(), pcol.size(), s));
+    CK(L.sell_pmap.upload(pmap.data(), pmap.size(), s));
+    CK(L.sell_pval.ensure((size_t)poff[ns] * 32));
+    L.sell_pslots = poff[ns];
+  }
+  CK(cudaStreamSynchronize(s));     // host index vectors go out of scope
+  L.n_slices = ns;
+  L.sell_dirty = true;
+  return ALEFSI_OK;
+}
+
+// refresh the sliced-ELL values after the CSR data changed
+void refresh_sell(Level& L, cudaStream_t s) {
+  if (L.n_slices == 0 || !L.sell_dirty) return;
+  launch_sell_pack(L.sell_slots * 32, 9, L.sell_map.p, L.data.p, L.sell_val.p, s);
+  if (L.sell_pslots > 0)
+    launch_sell_pack(L.sell_pslots * 32, 1, L.sell_pmap.p, L.pp_data.p, L.sell_pval.p, s);
+  L.sell_dirty = false;
+}
 
 }  // namespace
 
@@ -201,8 +285,16 @@ struct MgHandle {
   DevBuf<double> g_in, g_out;
   // GMRES workspace
   int v_cap = 0;
-  DevBuf<double> V, w, z, t, xb, bb, partial, tmp, tmp2, scal;
-  DevBuf<int> flag;
+  DevBuf<double> V, w, xb, bb, vin, vout, partial, tmp, tmp2, scal;
+  // device-resident GMRES state: control block, Hessenberg (v_cap x
+  // v_cap-1), rotations, g, residual history, back-substitution result
+  DevBuf<GmresCtl> ctl;
+  DevBuf<double> Hd, csd, snd, gd, resd, yd;
+  GmresCtl* ctl_host = nullptr;     // pinned
+  // one CUDA graph per solve: init -> while (Arnoldi step) -> solution
+  bool solve_valid = false;
+  cudaGraphExec_t solve_exec = nullptr;
+  int64_t n_init = 0, n_body = 0, n_fin = 0;
   double* pinned = nullptr;
   int64_t kernel_launches = 0;
 
@@ -219,6 +311,8 @@ struct MgHandle {
 
   ~MgHandle() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (solve_exec) cudaGraphExecDestroy(solve_exec);
+    if (ctl_host) cudaFreeHost(ctl_host);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_in) cudaEventDestroy(cap_in);
     if (cap_out) cudaEventDestroy(cap_out);
@@ -441,6 +535,7 @@ struct MgHandle {
 
   int factorize() {
     const std::vector<const void*> before = graph_buffers();
+    for (auto& L : lv) refresh_sell(L, stream);
     int rc = start_coarse_inverse();
     if (rc) {
       if (side_stream) cudaStreamSynchronize(side_stream);
@@ -492,7 +587,7 @@ struct MgHandle {
       CK(L.d.ensure(L.ndof()));
     }
     factorized = true;
-    if (graph_buffers() != before) graph_valid = false;
+    if (graph_buffers() != before) graph_valid = solve_valid = false;
     return ALEFSI_OK;
   }
 
@@ -502,22 +597,151 @@ struct MgHandle {
     if (v_cap < max_iter + 1) {
       CK(V.alloc((size_t)(max_iter + 1) * n));
       v_cap = max_iter + 1;
+      const int m = v_cap - 1;
+      CK(Hd.alloc((size_t)(m + 1) * m));
+      CK(csd.alloc(m));
+      CK(snd.alloc(m));
+      CK(gd.alloc(m + 1));
+      CK(resd.alloc(m + 1));
+      CK(yd.alloc(m + 1));
+      CK(tmp.alloc(m + 2));
+      CK(tmp2.alloc(m + 2));
+      CK(partial.alloc((size_t)kRedBlocks * (m + 2)));
+      solve_valid = false;
     }
     if (w.n != (size_t)n) {
       CK(w.alloc(n));
-      CK(z.alloc(n));
-      CK(t.alloc(n));
       CK(xb.alloc(n));
       CK(bb.alloc(n));
-    }
-    if (partial.n < (size_t)kRedBlocks * (max_iter + 2)) CK(partial.alloc((size_t)kRedBlocks * (max_iter + 2)));
-    if (tmp.n < (size_t)max_iter + 2) {
-      CK(tmp.alloc(max_iter + 2));
-      CK(tmp2.alloc(max_iter + 2));
+      CK(vin.alloc(n));
+      CK(vout.alloc(n));
+      solve_valid = false;
     }
     if (!scal.p) CK(scal.alloc(4));
-    if (!flag.p) CK(flag.alloc(1));
+    if (!ctl.p) CK(ctl.alloc(1));
+    if (!ctl_host) CK(cudaMallocHost(&ctl_host, sizeof(GmresCtl)));
     if (!pinned) CK(cudaMallocHost(&pinned, sizeof(double) * 1024));
+    return ALEFSI_OK;
+  }
+
+  // The three phases of a solve (reference linsolve.py:41-115), enqueued on
+  // `stream`: init (||b||, tolerance, v_0), one Arnoldi step (V-cycle on
+  // vin -> vout, w = A vout, classical Gram-Schmidt with the conditional
+  // second pass, v_{k+1}, Givens update and stopping test), and the
+  // solution x = M(V y).  Each returns the number of kernels it enqueued.
+  int64_t enqueue_init(cudaGraphConditionalHandle cond, int use_cond) {
+    return launch_gmres_init(ctl.p, bb.p, fine().ndof(), partial.p, scal.p, resd.p, gd.p, V.p,
+                             vin.p, cond, use_cond, stream);
+  }
+
+  int64_t enqueue_step(cudaGraphConditionalHandle cond, int use_cond) {
+    Level& F = fine();
+    const int64_t n = F.ndof();
+    const int64_t before = kernel_launches;
+    cycle(n_levels - 1, vin.p, vout.p);
+    int64_t c = kernel_launches - before;
+    kernel_launches = before;
+    int pr = prof_begin(0, n_levels - 1);
+    launch_spmv(F.mat(), vout.p, nullptr, w.p, 0, stream);
+    prof_end(pr);
+    pr = prof_begin(6, n_levels - 1);
+    int* flag = &ctl.p->flag;
+    const int mx = v_cap;     // k + 1 <= v_cap - 1
+    // first classical Gram-Schmidt pass: tmp[0..k] = V w, tmp[k+1] = w.w
+    c += 1 + launch_multi_dot(ctl.p, mx, V.p, n, w.p, n, partial.p, tmp.p, nullptr, stream);
+    c += launch_multi_axpy(ctl.p, V.p, n, tmp.p, w.p, n, partial.p, scal.p, nullptr, stream);
+    c += launch_arnoldi_finish(ctl.p, tmp.p, tmp2.p, scal.p, 0, stream);
+    // conditional second pass (device flag)
+    c += launch_multi_dot(ctl.p, mx, V.p, n, w.p, n, partial.p, tmp2.p, flag, stream);
+    c += launch_multi_axpy(ctl.p, V.p, n, tmp2.p, w.p, n, partial.p, scal.p, flag, stream);
+    c += launch_arnoldi_finish(ctl.p, tmp.p, tmp2.p, scal.p, 1, stream);
+    c += launch_scale_copy_slot(ctl.p, w.p, V.p, n, tmp.p, vin.p, n, stream);
+    c += launch_givens(ctl.p, tmp.p, Hd.p, csd.p, snd.p, gd.p, resd.p, cond, use_cond, stream);
+    prof_end(pr);
+    return c;
+  }
+
+  int64_t enqueue_solution() {
+    const int64_t n = fine().ndof();
+    int64_t c = launch_gmres_solution(ctl.p, Hd.p, gd.p, yd.p, V.p, n, vin.p, n, stream);
+    const int64_t before = kernel_launches;
+    cycle(n_levels - 1, vin.p, vout.p);
+    c += kernel_launches - before;
+    kernel_launches = before;
+    return c;
+  }
+
+  // capture init -> while(step) -> solution as one graph (conditional while
+  // node; the body's last kernel sets the condition)
+  int build_solve_graph() {
+    if (!cap_stream) {
+      CK(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&cap_in, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&cap_out, cudaEventDisableTiming));
+    }
+    if (solve_exec) {
+      cudaGraphExecDestroy(solve_exec);
+      solve_exec = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    CK(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    CK(cudaGraphConditionalHandleCreate(&cond, graph, 0, 0));
+    cudaStream_t user = stream;
+    stream = cap_stream;
+    auto restore = [&](cudaError_t e) {
+      stream = user;
+      if (e != cudaSuccess) cudaGraphDestroy(graph);
+      return e;
+    };
+    CK(restore(cudaStreamBeginCaptureToGraph(stream, graph, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal)));
+    stream = cap_stream;
+    n_init = enqueue_init(cond, 1);
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t cg = nullptr;
+    cudaError_t e = cudaStreamGetCaptureInfo(stream, &st, nullptr, &cg, &deps, &ndeps);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    if (e == cudaSuccess) e = cudaGraphAddNode(&wnode, cg, deps, ndeps, &cp);
+    if (e == cudaSuccess)
+      e = cudaStreamUpdateCaptureDependencies(stream, &wnode, 1, cudaStreamSetCaptureDependencies);
+    if (e != cudaSuccess) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(stream, &junk);
+      return fail(ALEFSI_ERR_CUDA, std::string("solve graph: ") + cudaGetErrorString(restore(e)));
+    }
+    // body: one Arnoldi step, captured from a second (private) stream
+    cudaStream_t body_stream;
+    e = cudaStreamCreateWithFlags(&body_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess)
+      e = cudaStreamBeginCaptureToGraph(body_stream, cp.conditional.phGraph_out[0], nullptr,
+                                        nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      stream = body_stream;
+      n_body = enqueue_step(cond, 1);
+      stream = cap_stream;
+      e = cudaStreamEndCapture(body_stream, nullptr);
+    }
+    cudaStreamDestroy(body_stream);
+    if (e != cudaSuccess) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(stream, &junk);
+      return fail(ALEFSI_ERR_CUDA, std::string("solve graph body: ") + cudaGetErrorString(restore(e)));
+    }
+    n_fin = enqueue_solution();
+    e = cudaStreamEndCapture(stream, &graph);
+    CK(restore(e));
+    e = cudaGraphInstantiate(&solve_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    solve_valid = true;
     return ALEFSI_OK;
   }
 
@@ -527,99 +751,57 @@ struct MgHandle {
     if (max_iter < 1 || max_iter > 510) return fail(ALEFSI_ERR_ARG, "max_iter must be in [1, 510]");
     int rc = ensure_workspace(max_iter);
     if (rc) return rc;
-    Level& F = fine();
-    const int64_t n = F.ndof();
-    const DevMatrix A = F.mat();
-    const double* b = b_in;
-    double* x = x_out;
-    if (host_ptrs) {
-      CK(cudaMemcpyAsync(bb.p, b_in, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
-      b = bb.p;
-      x = xb.p;
-    }
-    launch_sumsq(b, n, partial.p, scal.p, stream);
-    CK(cudaMemcpyAsync(pinned, scal.p, sizeof(double), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    const double beta = std::sqrt(pinned[0]);
-    residuals[0] = beta;
-    *iterations = 0;
-    *converged = 1;
-    const double tol = std::max(rel_tol * beta, abs_tol);
-    if (beta == 0.0 || beta <= tol) {
-      CK(cudaMemsetAsync(x, 0, sizeof(double) * n, stream));
-      if (host_ptrs)
-        CK(cudaMemcpyAsync(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      return ALEFSI_OK;
-    }
-    const int m = max_iter;
-    std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1, 0.0);
-    auto Hat = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
-    g[0] = beta;
-    launch_scale(b, V.p, beta, n, stream);
-    int k = 0;
-    double res = beta;
-    for (k = 0; k < m; ++k) {
-      double* vk = V.p + (size_t)k * n;
-      rc = apply(vk, z.p);
-      if (rc) return rc;
-      int pr = prof_begin(0, n_levels - 1);
-      launch_spmv(A, z.p, nullptr, w.p, 0, stream);
-      prof_end(pr);
-      pr = prof_begin(6, n_levels - 1);
-      // first classical Gram-Schmidt pass: tmp[0..k] = V w, tmp[k+1] = w.w
-      launch_multi_dot(k + 1, V.p, n, w.p, n, partial.p, tmp.p, nullptr, stream);
-      launch_multi_axpy(k + 1, V.p, n, tmp.p, w.p, n, partial.p, scal.p, nullptr, stream);
-      launch_arnoldi_finish(k, tmp.p, tmp2.p, tmp.p + k + 1, scal.p, flag.p, 0, stream);
-      // conditional second pass (device flag)
-      launch_multi_dot(k + 1, V.p, n, w.p, n, partial.p, tmp2.p, flag.p, stream);
-      launch_multi_axpy(k + 1, V.p, n, tmp2.p, w.p, n, partial.p, scal.p, flag.p, stream);
-      launch_arnoldi_finish(k, tmp.p, tmp2.p, tmp.p + k + 1, scal.p, flag.p, 1, stream);
-      launch_scale_copy(w.p, V.p + (size_t)(k + 1) * n, tmp.p + k + 1, n, stream);
-      prof_end(pr);
-      kernel_launches += 14;
-      CK(cudaMemcpyAsync(pinned, tmp.p, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      prof_collect();
-      for (int i = 0; i <= k + 1; ++i) Hat(i, k) = pinned[i];
-      // accumulated Givens rotations, then the new one (linsolve.py:88-98)
-      for (int i = 0; i < k; ++i) {
-        const double tt = cs[i] * Hat(i, k) + sn[i] * Hat(i + 1, k);
-        Hat(i + 1, k) = -sn[i] * Hat(i, k) + cs[i] * Hat(i + 1, k);
-        Hat(i, k) = tt;
+    const int64_t n = fine().ndof();
+    GmresCtl& hc = *ctl_host;
+    hc = GmresCtl{};
+    hc.rel_tol = rel_tol;
+    hc.abs_tol = abs_tol;
+    hc.max_iter = max_iter;
+    hc.hstride = v_cap - 1;
+    CK(cudaMemcpyAsync(ctl.p, &hc, sizeof(GmresCtl), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(bb.p, b_in, sizeof(double) * n,
+                       host_ptrs ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, stream));
+    if (use_graph && !prof_on) {
+      if (!solve_valid) {
+        rc = build_solve_graph();
+        if (rc) return rc;
       }
-      const double r = std::hypot(Hat(k, k), Hat(k + 1, k));
-      cs[k] = Hat(k, k) / r;
-      sn[k] = Hat(k + 1, k) / r;
-      Hat(k, k) = r;
-      Hat(k + 1, k) = 0.0;
-      g[k + 1] = -sn[k] * g[k];
-      g[k] = cs[k] * g[k];
-      res = std::fabs(g[k + 1]);
-      residuals[k + 1] = res;
-      if (res <= tol) break;
+      CK(cudaGraphLaunch(solve_exec, stream));
+      CK(cudaMemcpyAsync(&hc, ctl.p, sizeof(GmresCtl), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      kernel_launches += n_init + (int64_t)hc.its * n_body + n_fin;
+    } else {
+      // the same kernels, stepped from the host (per-kernel profiling, or
+      // graphs off): one control-block read per Arnoldi step
+      cudaGraphConditionalHandle none = 0;
+      kernel_launches += enqueue_init(none, 0);
+      CK(cudaMemcpyAsync(&hc, ctl.p, sizeof(GmresCtl), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      while (!hc.done) {
+        kernel_launches += enqueue_step(none, 0);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&hc, ctl.p, sizeof(GmresCtl), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        prof_collect();
+      }
+      kernel_launches += enqueue_solution();
     }
-    const int its = std::min(k + 1, m);
-    *iterations = its;
-    // y = triu(H)^{-1} g, column-oriented back substitution
-    std::vector<double> y(g.begin(), g.begin() + its);
-    for (int j = its - 1; j >= 0; --j) {
-      y[j] /= Hat(j, j);
-      for (int i = 0; i < j; ++i) y[i] -= y[j] * Hat(i, j);
+    CK(cudaGetLastError());
+    const int its = hc.its;
+    if (its == 0) {       // ||b|| <= tol: x = 0 (linsolve.py:58-61)
+      if (host_ptrs) std::fill(x_out, x_out + n, 0.0);
+      else CK(cudaMemsetAsync(x_out, 0, sizeof(double) * n, stream));
+    } else {
+      CK(cudaMemcpyAsync(x_out, vout.p, sizeof(double) * n,
+                         host_ptrs ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, stream));
     }
-    for (int i = 0; i < its; ++i) pinned[i] = y[i];
-    CK(cudaMemcpyAsync(tmp.p, pinned, sizeof(double) * its, cudaMemcpyHostToDevice, stream));
-    launch_combine(its, V.p, n, tmp.p, t.p, n, stream);
-    rc = apply(t.p, x);
-    if (rc) return rc;
-    if (host_ptrs)
-      CK(cudaMemcpyAsync(x_out, x, sizeof(double) * n, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(residuals, resd.p, sizeof(double) * (its + 1), cudaMemcpyDeviceToHost,
+                       stream));
     CK(cudaStreamSynchronize(stream));
     prof_collect();
-    if (res > tol) {
-      *converged = 0;
-      return fail(ALEFSI_ERR_NOT_CONVERGED, "GMRES did not reach the tolerance");
-    }
+    *iterations = its;
+    *converged = hc.converged;
+    if (!hc.converged) return fail(ALEFSI_ERR_NOT_CONVERGED, "GMRES did not reach the tolerance");
     return ALEFSI_OK;
   }
 };
@@ -701,6 +883,7 @@ int alefsi_mg_set_stream(alefsi_mg h, void* stream) {
   m->stream = reinterpret_cast<cudaStream_t>(stream);
   m->own_stream = false;
   m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
 }
 
@@ -709,6 +892,7 @@ int alefsi_mg_use_graph(alefsi_mg h, int32_t on) {
   if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
   m->use_graph = on != 0;
   m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
 }
 
@@ -736,6 +920,9 @@ int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nn
     CKAPI(L.pp_indices.upload(pp_indices, nnz_pp, m->stream));
     CKAPI(L.pp_data.upload(pp_data, nnz_pp, m->stream));
   }
+  L.nc = nc;
+  rc = alefsi::build_sell(L, indptr, indices, pp_indptr, pp_indices, m->stream);
+  if (rc) return rc;
   if (level == 0) {
     const int64_t n0 = n_nodes * nc;
     if (n0 > 20000) return fail(ALEFSI_ERR_ARG, "coarse level too large for a dense inverse");
@@ -757,6 +944,7 @@ int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nn
   L.has_matrix = true;
   m->factorized = false;
   m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }
@@ -785,11 +973,15 @@ int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t n
     CKAPI(L.pp_data.alloc(nnz_pp));
     CKAPI(cudaMemsetAsync(L.pp_data.p, 0, sizeof(double) * nnz_pp, m->stream));
   }
+  L.nc = nc;
+  rc = alefsi::build_sell(L, indptr, indices, pp_indptr, pp_indices, m->stream);
+  if (rc) return rc;
   L.host_dense.clear();
   CKAPI(cudaStreamSynchronize(m->stream));
   L.has_matrix = true;
   m->factorized = false;
   m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }
@@ -866,6 +1058,7 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
   CKAPI(cudaMemsetAsync(L.data.p, 0, sizeof(double) * L.nnzb * nc * nc, s));
   if (L.nnz_pp > 0) CKAPI(cudaMemsetAsync(L.pp_data.p, 0, sizeof(double) * L.nnz_pp, s));
   CKAPI(cudaMemsetAsync(m->status.p, 0, sizeof(int64_t), s));
+  L.sell_dirty = true;
   alefsi::AsmArgs a;
   a.cell_nodes = L.asm_cell_nodes.p;
   a.coords = L.asm_coords.p;
@@ -1160,6 +1353,7 @@ int alefsi_mg_set_patches(alefsi_mg h, int32_t level, int32_t n_groups,
   CKAPI(cudaStreamSynchronize(m->stream));
   m->factorized = false;
   m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }
@@ -1200,6 +1394,7 @@ int alefsi_mg_set_prolongation(alefsi_mg h, int32_t level, int64_t n_fine, int64
   L.n_coarse = n_coarse;
   L.has_P = true;
   m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }
@@ -1214,6 +1409,7 @@ int alefsi_mg_set_constrained(alefsi_mg h, int32_t level, const uint8_t* mask) {
   CKAPI(L.constrained.upload(mask, L.ndof(), m->stream));
   CKAPI(cudaStreamSynchronize(m->stream));
   m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }
@@ -1248,6 +1444,7 @@ int alefsi_mg_spmv(alefsi_mg h, int32_t level, const double* x, const double* b,
   MgHandle* m = H(h);
   int rc = check_level(m, level);
   if (rc) return rc;
+  alefsi::refresh_sell(m->lv[level], m->stream);
   alefsi::launch_spmv(m->lv[level].mat(), x, b, y, b ? 1 : 0, m->stream);
   CKAPI(cudaGetLastError());
   return ALEFSI_OK;
