@@ -1,7 +1,8 @@
-"""Run the unmodified reference (``/root/reference/pkg/src/alefsi``) on a
-workload definition.  Only available in the build container, where the
-reference is mounted; tests using it are skipped elsewhere.  Also used by
-``tests/golden/make_golden.py`` to generate the committed fixtures."""
+"""Run the unmodified reference on a workload definition: the read-only
+source tree ``/root/reference/pkg/src/alefsi`` in the build container, else
+the copy installed into ``baseline/_ref`` (which travels to the GPU box).
+Also used by ``tests/golden/make_golden.py`` to generate the committed
+fixtures."""
 
 from __future__ import annotations
 
@@ -11,6 +12,10 @@ import sys
 import numpy as np
 
 REF_SRC = "/root/reference/pkg/src"
+if not os.path.isdir(os.path.join(REF_SRC, "alefsi")):
+    # GPU box: the unmodified reference installed into baseline/_ref travels
+    REF_SRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           "baseline", "_ref")
 AVAILABLE = os.path.isdir(os.path.join(REF_SRC, "alefsi"))
 
 

@@ -19,10 +19,12 @@ from paper_1904_02401_b200 import mesh as mm, workloads as W  # noqa: E402
 def test_bench_golden_gate_rejects_a_wrong_history():
     """bench.py refuses to print a line whose warm-up history differs from
     the committed golden."""
-    g, _ = load_golden("3d_large_oracle")
+    g, _ = load_golden("3d_large")
     ok = bench.check_against_golden("3d_large", g["iterations"], g["residuals"],
                                     g["x_checksums"])
-    assert ok["source"].endswith("3d_large_oracle.json")
+    assert ok["source"].endswith("3d_large.json")      # the reference's own run
+    go, _ = load_golden("3d_large_oracle")             # the pinned oracle agrees
+    bench.check_against_golden("3d_large", go["iterations"], go["residuals"], go["x_checksums"])
     bad = list(g["residuals"])
     bad[3] *= 1 + 1e-8
     with pytest.raises(bench.ParityError):
