@@ -76,6 +76,14 @@ SPECS = {
     "3d_large": dict(dim=3, lengths=(4.0, 1.0, 1.0), coarse=(8, 2, 2), levels=5, taper=0.0),
     "2d_mini": dict(dim=2, lengths=(4.0, 1.0), coarse=(8, 2), levels=3, taper=0.0),
     "3d_mini": dict(dim=3, lengths=(4.0, 1.0, 1.0), coarse=(8, 2, 2), levels=3, taper=0.0),
+    # the reference's 3D default blocking (one-element fluid, 2x2x2-cell solid
+    # macros) on a corner solid block nested in the coarse grid
+    "3d_large_refblock": dict(dim=3, lengths=(4.0, 1.0, 1.0), coarse=(8, 2, 2), levels=5,
+                              taper=0.0, solid=((1.0, 0.0, 0.0), (2.0, 0.5, 0.5)),
+                              patches=("one", "multi")),
+    "3d_mini_refblock": dict(dim=3, lengths=(4.0, 1.0, 1.0), coarse=(8, 2, 2), levels=3,
+                             taper=0.0, solid=((1.0, 0.0, 0.0), (2.0, 0.5, 0.5)),
+                             patches=("one", "multi")),
 }
 DT = 0.01
 THETA = 0.5 + 2.0 * DT          # shifted Crank-Nicolson (reference newton.py:69-74)
@@ -84,9 +92,9 @@ MAX_ITER = 250
 SOLID_SNAP = 0.125
 
 
-def solid_box(dim):
-    lo = np.array([1.0, 0.4, 0.4][:dim])
-    hi = np.array([2.0, 0.6, 0.6][:dim])
+def solid_box(dim, box=None):
+    lo = np.array(box[0] if box else [1.0, 0.4, 0.4][:dim])
+    hi = np.array(box[1] if box else [2.0, 0.6, 0.6][:dim])
     s = SOLID_SNAP
     return np.floor(lo / s + 1e-9) * s, np.ceil(hi / s - 1e-9) * s
 
@@ -167,7 +175,7 @@ def linearisation_state(spec, X, node_class, node_fluid=0):
     U[:, 1:1 + d] = sine_field(rng, X, spec["lengths"], d)
     u = 0.01 * sine_field(rng, X, spec["lengths"], d)
     if spec["taper"] > 0:
-        lo, hi = solid_box(d)
+        lo, hi = solid_box(d, spec.get("solid"))
         gap = np.maximum(np.maximum(lo - X, X - hi), 0.0)
         phi = np.maximum(0.0, 1.0 - np.linalg.norm(gap, axis=1) / spec["taper"])
         phi[node_class != node_fluid] = 1.0
@@ -247,7 +255,7 @@ def build(name, setup_threads=1, log=None, min_batch=4096):
     v, c, s, f = box_arrays(spec["lengths"], spec["coarse"])
     coarse = a.mesh.MeshLevel(d, v, c, s, f)
     h = a.mesh.build_hierarchy(coarse, spec["levels"] - 1)
-    lo, hi = solid_box(d)
+    lo, hi = solid_box(d, spec.get("solid"))
     for m in h.levels:
         cen = m.vertices[m.cells].mean(axis=1)
         inside = np.all((cen > lo) & (cen < hi), axis=1)
@@ -257,8 +265,9 @@ def build(name, setup_threads=1, log=None, min_batch=4096):
     flags = a.problem.FsiFlags(lps_dt=DT)
     one, multi = a.mesh.ONE_ELEMENT, a.mesh.MULTI_ELEMENT
     strat = multi if d == 2 else one
+    fp, sp_ = spec.get("patches", (strat, strat))
     cfg = a.newton.LinearConfig(momentum_rel_tol=REL_TOL, max_iter=MAX_ITER, nu_pre=2,
-                                nu_post=2, omega=0.8, fluid_patches=strat, solid_patches=strat)
+                                nu_post=2, omega=0.8, fluid_patches=fp, solid_patches=sp_)
     with threaded_einsum(setup_threads, min_batch):
         prob = a.problem.FsiProblem(h, mats, flags)
         t1 = time.perf_counter()

@@ -131,6 +131,18 @@ CONFIGS = {
     # 16x4x4 fine, solid block against the y=0/z=0 walls: smallest 3D case with solid
     "3d_tiny": Workload("3d_tiny", 3, (4.0, 1.0, 1.0), (4, 1, 1), 3, (1.0, 0.0, 0.0),
                         (2.0, 0.5, 0.5)),
+    # the reference's 3D default blocking (newton.py:53-56: one-element fluid
+    # patches, 2x2x2-cell solid macro patches = 500x500 blocks) at the config-3
+    # mesh.  The BASELINE solid box is not nested in the coarse grid (its
+    # level-2 macros mix fluid and solid cells and the reference's own
+    # MG-GMRES stalls: 3d_mini, 60 iterations, residual 1.6 of 23.5), so the
+    # solid block sits in a corner aligned with the coarsest grid
+    "3d_large_refblock": Workload("3d_large_refblock", 3, (4.0, 1.0, 1.0), (8, 2, 2), 5,
+                                  (1.0, 0.0, 0.0), (2.0, 0.5, 0.5), fluid_patches="one",
+                                  solid_patches="multi"),
+    "3d_mini_refblock": Workload("3d_mini_refblock", 3, (4.0, 1.0, 1.0), (8, 2, 2), 3,
+                                 (1.0, 0.0, 0.0), (2.0, 0.5, 0.5), fluid_patches="one",
+                                 solid_patches="multi"),
     # the reference's 3D default blocking: one-element fluid patches (108x108)
     # and 2x2x2-cell solid patches (500x500), on a solid slab that is nested
     # on every level (the 3d_tiny block is not: its level-1 solid macros

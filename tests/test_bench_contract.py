@@ -59,7 +59,8 @@ def test_ref_arm_workload_is_the_device_workload(name):
         np.testing.assert_array_equal(arr, m.facets[key])
     assert set(f) == {k for k, a in m.facets.items() if len(a)}
     assert spec["levels"] == wl.n_levels and spec["taper"] == wl.deform_taper
-    lo, hi = ref_arm.solid_box(spec["dim"])
+    lo, hi = ref_arm.solid_box(spec["dim"], spec.get("solid"))
+    assert tuple(spec.get("patches", wl.patch_strategies())) == wl.patch_strategies()
     wlo, whi = wl.solid_box()
     np.testing.assert_array_equal(lo, wlo)
     np.testing.assert_array_equal(hi, whi)
