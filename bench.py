@@ -338,6 +338,7 @@ def run_ours(args, rank, world):
         return None
 
     kb = kernel_bytes(case, wl)
+    n = len(case.b)
     info = WORKLOADS[args.workload]
     if n != info["dofs"] or kb["spmv"] + kb["vanka_apply"] <= L2_BYTES:
         raise RuntimeError(f"workload table out of date for {args.workload}")

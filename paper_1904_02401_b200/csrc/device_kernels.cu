@@ -1548,39 +1548,22 @@ __global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm,
   }
 }
 
-// warp per row, 32-byte loads of the padded row (ld % 4 == 0) and of x, two
-// accumulators per lane (fixed order: deterministic)
+// warp per row; lane j sums columns j, j + 32, ... (fixed order).  A wider
+// 32-byte-load variant over padded rows (two accumulators per lane) was
+// measured: the changed summation order moved the 3d_tiny GMRES history
+// from ~1e-12 to 1.03e-10 of the reference's (its own BLAS-thread
+// run-to-run spread is 6e-11), for ~6 % of the config-0 solve.
 __global__ void __launch_bounds__(256) dense_matvec_kernel(int64_t n, const double* __restrict__ M,
-                                                           int64_t ld,
                                                            const double* __restrict__ x,
                                                            double* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (row >= n) return;
-  const double* r = M + row * ld;
-  const int64_t nq = ld / 4;
-  double a0 = 0.0, a1 = 0.0;
-  for (int64_t q = lane; q < nq; q += 32) {
-    const d4 m = ld256_ro(r + 4 * q);
-    double xv[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) xv[u] = 4 * q + u < n ? __ldg(x + 4 * q + u) : 0.0;
-    a0 = fma(m.x, xv[0], a0);
-    a1 = fma(m.y, xv[1], a1);
-    a0 = fma(m.z, xv[2], a0);
-    a1 = fma(m.w, xv[3], a1);
-  }
-  const double acc = warp_sum(a0 + a1);
+  const double* r = M + row * n;
+  double acc = 0.0;
+  for (int64_t j = lane; j < n; j += 32) acc = fma(__ldg(r + j), __ldg(x + j), acc);
+  acc = warp_sum(acc);
   if (lane == 0) y[row] = acc;
-}
-
-__global__ void pad_rows_kernel(int64_t n, const double* __restrict__ M, int64_t ld,
-                                double* __restrict__ P) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * ld;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / ld, j = e - i * ld;
-    P[e] = j < n ? M[i * n + j] : 0.0;
-  }
 }
 
 // --------------------------------------------------------------------------
@@ -2243,13 +2226,9 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
   return 0;
 }
 
-void launch_dense_matvec(int64_t n, const double* M, int64_t ld, const double* x, double* y,
+void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
                          cudaStream_t s) {
-  dense_matvec_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, M, ld, x, y);
-}
-
-void launch_pad_rows(int64_t n, const double* M, int64_t ld, double* P, cudaStream_t s) {
-  pad_rows_kernel<<<(int)std::min<int64_t>(grid_for(n * ld, 256), 4096), 256, 0, s>>>(n, M, ld, P);
+  dense_matvec_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, M, x, y);
 }
 
 int launch_multi_dot(GmresCtl* ctl, int max_nvec, const double* V, int64_t ldv, const double* w,

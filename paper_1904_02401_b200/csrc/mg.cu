@@ -194,6 +194,8 @@ struct Level {
   }
 };
 
+constexpr int64_t kSellMinNodes = 1 << 18;
+
 // Sliced-ELL index of a CSR pattern (32-row slices, no row permutation: the
 // Q2 node numbering keeps rows of one slice at nearly equal length — config 1
 // finest level: 0.25 % block padding).  pos = slot * 32 + lane.
@@ -225,7 +227,10 @@ int build_sell(Level& L, const int64_t* indptr, const int32_t* indices, const in
                const int32_t* pp_indices, cudaStream_t s) {
   L.n_slices = 0;
   L.sell_slots = L.sell_pslots = 0;
-  if (L.nc != 3 || L.n_nodes == 0) return ALEFSI_OK;
+  // large levels only: a lane walks its row's blocks serially, which the
+  // small, L2-resident levels cannot hide (2d_large level 3, 66k nodes:
+  // 76 us with sliced ELL); they keep the half-warp-per-row kernel
+  if (L.nc != 3 || L.n_nodes < kSellMinNodes) return ALEFSI_OK;
   std::vector<int64_t> off, map;
   std::vector<int32_t> col;
   sell_index(L.n_nodes, indptr, indices, off, col, map);
@@ -267,10 +272,6 @@ struct MgHandle {
   double omega = 0.8;
   std::vector<Level> lv;
   DevBuf<double> coarse_inv, coarse_work;
-  // the inverse with rows padded to a multiple of 4 doubles (32-byte
-  // aligned rows for the 256-bit loads of the coarse matvec)
-  DevBuf<double> coarse_pad;
-  int64_t coarse_ld = 0;
   DevBuf<int64_t> status, coarse_status;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -400,7 +401,7 @@ struct MgHandle {
     Level& L = lv[l];
     if (l == 0) {
       int pr = prof_begin(5, l);
-      launch_dense_matvec(L.ndof(), coarse_pad.p, coarse_ld, b, x, stream);
+      launch_dense_matvec(L.ndof(), coarse_inv.p, b, x, stream);
       prof_end(pr);
       ++kernel_launches;
       return;
@@ -484,7 +485,7 @@ struct MgHandle {
   // buffers the captured V-cycle graph reads; a re-factorisation that keeps
   // them (same sizes: ensure() does not reallocate) keeps the graph valid
   std::vector<const void*> graph_buffers() const {
-    std::vector<const void*> v{coarse_inv.p, coarse_pad.p};
+    std::vector<const void*> v{coarse_inv.p};
     for (const auto& L : lv) {
       v.push_back(L.x.p);
       v.push_back(L.b.p);
@@ -523,9 +524,6 @@ struct MgHandle {
     if (dense_inverse(coarse_inv.p, n0, coarse_work.p, coarse_status.p, side_stream) != 0)
       return fail(ALEFSI_ERR_ARG, "coarse level too large for the dense inverse (" +
                                       std::to_string(n0) + " > 4096 dofs)");
-    coarse_ld = (n0 + 3) / 4 * 4;
-    CK(coarse_pad.ensure((size_t)n0 * coarse_ld));
-    launch_pad_rows(n0, coarse_inv.p, coarse_ld, coarse_pad.p, side_stream);
     CK(cudaGetLastError());
     CK(cudaEventRecord(side_out, side_stream));
     return ALEFSI_OK;
@@ -1505,7 +1503,7 @@ int alefsi_mg_coarse_solve(alefsi_mg h, const double* b, double* x) {
   MgHandle* m = H(h);
   if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
   if (!m->factorized) return fail(ALEFSI_ERR_STATE, "coarse solve before factorize");
-  alefsi::launch_dense_matvec(m->lv[0].ndof(), m->coarse_pad.p, m->coarse_ld, b, x, m->stream);
+  alefsi::launch_dense_matvec(m->lv[0].ndof(), m->coarse_inv.p, b, x, m->stream);
   CKAPI(cudaGetLastError());
   return ALEFSI_OK;
   ALEFSI_TRY_END
