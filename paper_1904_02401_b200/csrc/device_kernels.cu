@@ -55,6 +55,33 @@ constexpr int64_t kSmallPatchCount = 8192;
 
 inline int grid_for(int64_t n, int per_block) { return (int)((n + per_block - 1) / per_block); }
 
+// Programmatic dependent launch: kernels of the solve path are launched with
+// programmaticStreamSerialization, so a kernel's CTAs may be scheduled while
+// its predecessor on the stream (or graph edge) drains.  pdl_entry() lets the
+// next kernel launch early and then waits until the predecessor's grid has
+// completed and its memory is visible — before this kernel reads or writes
+// anything — so the ordering is the plain stream order minus the launch gap.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // --------------------------------------------------------------------------
 // Block-sparse matrix-vector product.  One warp per block row (mesh node).
 // NC = 4: lane = 4*blk + r, each lane streams one 32-byte block row
@@ -73,6 +100,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t n, const int64_t* __r
                                                    const double* __restrict__ x,
                                                    const double* __restrict__ b,
                                                    double* __restrict__ y) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (row >= n) return;
@@ -148,6 +176,7 @@ __global__ void __launch_bounds__(256) spmv32_kernel(int64_t n, const int64_t* _
                                                      const double* __restrict__ x,
                                                      const double* __restrict__ b,
                                                      double* __restrict__ y) {
+  pdl_entry();
   static_assert(NC % 2 == 0 && kWarp % NC == 0, "even block size");
   constexpr int BPI = kWarp / NC, H = NC / 2;
   const int lane = threadIdx.x & 31;
@@ -223,6 +252,7 @@ __global__ void __launch_bounds__(256) spmv4_kernel(int64_t n, const int64_t* __
                                                        const double* __restrict__ x,
                                                        const double* __restrict__ b,
                                                        double* __restrict__ y) {
+  pdl_entry();
   constexpr int NC = 4, BPI = kWarp / NC;
   const int lane = threadIdx.x & 31;
   const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -276,6 +306,7 @@ __global__ void __launch_bounds__(256) spmv_half_kernel(int64_t n, const int64_t
                                                         const double* __restrict__ x,
                                                         const double* __restrict__ b,
                                                         double* __restrict__ y) {
+  pdl_entry();
   constexpr int HL = 16, BPI = HL / NC;
   const int lane = threadIdx.x & 31, hl = lane & (HL - 1);
   const unsigned hmask = (lane < HL) ? 0x0000ffffu : 0xffff0000u;
@@ -333,6 +364,7 @@ __global__ void __launch_bounds__(256) spmv3_sell_kernel(int64_t n, int64_t n_sl
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ b,
                                                          double* __restrict__ y) {
+  pdl_entry();
   constexpr int NC = 3;
   const int lane = threadIdx.x & 31;
   const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -415,6 +447,7 @@ struct ApplyGroups {
 template <int NP, int LD, int NC, int RPT>
 __global__ void __launch_bounds__(ApplyShape<LD, RPT>::BLK) vanka_apply_kernel(
     ApplyGroups G, const double* __restrict__ d) {
+  pdl_entry();
   constexpr int NPN = NP / NC;
   constexpr int TPP = ApplyShape<LD, RPT>::TPP;
   constexpr int PPC = ApplyShape<LD, RPT>::PPC;
@@ -473,6 +506,7 @@ __global__ void __launch_bounds__(ApplyShape<LD, RPT>::BLK) vanka_apply_kernel(
 template <int NP, int LD, int NC, int RPT, int S>
 __global__ void __launch_bounds__(ApplyShape<LD, RPT>::TPP * S) vanka_apply_split_kernel(
     ApplyGroups G, const double* __restrict__ d) {
+  pdl_entry();
   constexpr int NPN = NP / NC;
   constexpr int TPP = ApplyShape<LD, RPT>::TPP;
   constexpr int CPS = (NP + S - 1) / S;   // columns per split
@@ -533,6 +567,7 @@ __global__ void vanka_gather_kernel(int64_t ndof, int nc, const int64_t* __restr
                                     const int64_t* __restrict__ goff,
                                     const double* __restrict__ w, const double* __restrict__ Y,
                                     double* __restrict__ x, double omega, int init_zero) {
+  pdl_entry();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ndof) return;
   const int64_t n = t / nc;
@@ -554,6 +589,7 @@ __global__ void vanka_gather4_kernel(int64_t n_nodes, const int64_t* __restrict_
                                      const int64_t* __restrict__ goff,
                                      const double* __restrict__ w, const double* __restrict__ Y,
                                      double* __restrict__ x, double omega, int init_zero) {
+  pdl_entry();
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= n_nodes) return;
   const double wn = __ldg(w + n);
@@ -898,6 +934,7 @@ __global__ void transfer_kernel(int64_t nrows, int nc, const int64_t* __restrict
                                 const double* __restrict__ src,
                                 const uint8_t* __restrict__ constrained,
                                 double* __restrict__ dst, int add) {
+  pdl_entry();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nrows * nc) return;
   const int64_t row = t / nc;
@@ -933,6 +970,7 @@ __global__ void __launch_bounds__(256) transfer_split_kernel(
     int64_t nrows, int nc, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
     const double* __restrict__ val, const double* __restrict__ src,
     const uint8_t* __restrict__ constrained, double* __restrict__ dst, int add) {
+  pdl_entry();
   const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int k = threadIdx.x & 7;
   const bool live = g < nrows * nc;
@@ -960,6 +998,7 @@ __global__ void transfer4_kernel(int64_t nrows, const int64_t* __restrict__ ptr,
                                  const double* __restrict__ src,
                                  const uint8_t* __restrict__ constrained,
                                  double* __restrict__ dst, int add) {
+  pdl_entry();
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= nrows) return;
   const int64_t beg = ptr[row], end = ptr[row + 1];
@@ -1556,6 +1595,7 @@ __global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm,
 __global__ void __launch_bounds__(256) dense_matvec_kernel(int64_t n, const double* __restrict__ M,
                                                            const double* __restrict__ x,
                                                            double* __restrict__ y) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (row >= n) return;
@@ -1582,6 +1622,7 @@ __global__ void __launch_bounds__(256) multi_dot_kernel(const GmresCtl* __restri
                                                         int64_t ldv, const double* __restrict__ w,
                                                         int64_t n, double* __restrict__ partial,
                                                         const int* flag) {
+  pdl_entry();
   if (flag != nullptr && *flag == 0) return;
   __shared__ double red[8];
   const int nvec = ctl->k + 1;            // basis vectors v_0 .. v_k
@@ -1638,6 +1679,7 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(int nout, int nblo
                                                               double* __restrict__ out,
                                                               const int* flag,
                                                               const GmresCtl* ctl) {
+  pdl_entry();
   if (flag != nullptr && *flag == 0) return;
   if (ctl != nullptr) nout = ctl->k + 2;
   const int j = blockIdx.x;
@@ -1656,6 +1698,7 @@ __global__ void __launch_bounds__(256) multi_axpy_kernel(const GmresCtl* __restr
                                                          double* __restrict__ w, int64_t n,
                                                          double* __restrict__ partial,
                                                          const int* flag) {
+  pdl_entry();
   if (flag != nullptr && *flag == 0) return;
   __shared__ double hs[512];
   __shared__ double red[8];
@@ -1709,6 +1752,7 @@ __global__ void __launch_bounds__(256) multi_axpy_kernel(const GmresCtl* __restr
 // H[k+1, k] = ||w||.
 __global__ void arnoldi_finish_kernel(GmresCtl* ctl, double* hcol, const double* h2,
                                       const double* na2, int stage) {
+  pdl_entry();
   const int k = ctl->k;
   if (stage == 0) {
     if (threadIdx.x == 0) ctl->flag = (sqrt(*na2) < 0.7071 * sqrt(hcol[k + 1])) ? 1 : 0;
@@ -1726,6 +1770,7 @@ __global__ void scale_copy_slot_kernel(const GmresCtl* __restrict__ ctl,
                                        const double* __restrict__ w, double* __restrict__ V,
                                        int64_t ldv, const double* __restrict__ hcol,
                                        double* __restrict__ vin, int64_t n) {
+  pdl_entry();
   const int k = ctl->k;
   const double h = hcol[k + 1];
   if (!(h > 0.0)) return;
@@ -1741,6 +1786,7 @@ __global__ void scale_copy_slot_kernel(const GmresCtl* __restrict__ ctl,
 // beta = ||b||, tolerance, early exit (linsolve.py:55-60); v_0 = b / beta
 __global__ void gmres_init_kernel(GmresCtl* ctl, const double* bb, double* res, double* g,
                                   cudaGraphConditionalHandle cond, int use_cond) {
+  pdl_entry();
   const double beta = sqrt(*bb);
   const double tol = fmax(ctl->rel_tol * beta, ctl->abs_tol);
   const int stop = (beta == 0.0 || beta <= tol) ? 1 : 0;
@@ -1757,6 +1803,7 @@ __global__ void gmres_init_kernel(GmresCtl* ctl, const double* bb, double* res, 
 
 __global__ void scale_dual_kernel(const GmresCtl* __restrict__ ctl, const double* __restrict__ b,
                                   double* __restrict__ v0, double* __restrict__ vin, int64_t n) {
+  pdl_entry();
   if (ctl->done) return;
   const double beta = ctl->beta;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1773,6 +1820,7 @@ __global__ void scale_dual_kernel(const GmresCtl* __restrict__ ctl, const double
 __global__ void givens_kernel(GmresCtl* ctl, const double* __restrict__ hcol, double* H,
                               double* cs, double* sn, double* g, double* res,
                               cudaGraphConditionalHandle cond, int use_cond) {
+  pdl_entry();
   const int k = ctl->k, m = ctl->hstride;
   auto Hat = [&](int i, int j) -> double& { return H[(int64_t)i * m + j]; };
   for (int i = 0; i <= k + 1; ++i) Hat(i, k) = hcol[i];
@@ -1802,6 +1850,7 @@ __global__ void givens_kernel(GmresCtl* ctl, const double* __restrict__ hcol, do
 // y = triu(H)^{-1} g (linsolve.py:107), column-oriented back substitution
 __global__ void backsolve_kernel(const GmresCtl* ctl, const double* H, const double* g,
                                  double* y) {
+  pdl_entry();
   const int its = ctl->its, m = ctl->hstride;
   for (int j = 0; j < its; ++j) y[j] = g[j];
   for (int j = its - 1; j >= 0; --j) {
@@ -1814,6 +1863,7 @@ __global__ void backsolve_kernel(const GmresCtl* ctl, const double* H, const dou
 __global__ void combine_kernel(const GmresCtl* __restrict__ ctl, const double* __restrict__ V,
                                int64_t ldv, const double* __restrict__ c, double* __restrict__ y,
                                int64_t n) {
+  pdl_entry();
   __shared__ double cs[512];
   const int nvec = ctl->its;
   for (int j = threadIdx.x; j < nvec; j += blockDim.x) cs[j] = c[j];
@@ -1828,6 +1878,7 @@ __global__ void combine_kernel(const GmresCtl* __restrict__ ctl, const double* _
 
 __global__ void __launch_bounds__(256) sumsq_kernel(const double* __restrict__ x, int64_t n,
                                                     double* __restrict__ partial) {
+  pdl_entry();
   __shared__ double red[8];
   double sq = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1845,21 +1896,21 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
     if (A.sell_off != nullptr) {
       const int sgrid = grid_for(A.n_slices * 32, 256);
       if (mode == 0)
-        spmv3_sell_kernel<0><<<sgrid, 256, 0, s>>>(A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
+        launch_pdl(spmv3_sell_kernel<0>, sgrid, 256, 0, s, A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
                                                    A.sell_val, A.sell_poff, A.sell_pcol,
                                                    A.sell_pval, x, b, y);
       else
-        spmv3_sell_kernel<1><<<sgrid, 256, 0, s>>>(A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
+        launch_pdl(spmv3_sell_kernel<1>, sgrid, 256, 0, s, A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
                                                    A.sell_val, A.sell_poff, A.sell_pcol,
                                                    A.sell_pval, x, b, y);
       return;
     }
     const int hgrid = grid_for(A.n_nodes * 16, 256);
     if (mode == 0)
-      spmv_half_kernel<NC, 0><<<hgrid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+      launch_pdl(spmv_half_kernel<NC, 0>, hgrid, 256, 0, s, A.n_nodes, A.indptr, A.indices, A.data,
                                                     A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
     else
-      spmv_half_kernel<NC, 1><<<hgrid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+      launch_pdl(spmv_half_kernel<NC, 1>, hgrid, 256, 0, s, A.n_nodes, A.indptr, A.indices, A.data,
                                                     A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
     return;
   }
@@ -1870,25 +1921,25 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
       const bool unr = A.n_nodes < kSmallLevelNodes;
       auto k = unr ? (mode == 0 ? spmv4_kernel<0, true> : spmv4_kernel<1, true>)
                    : (mode == 0 ? spmv4_kernel<0, false> : spmv4_kernel<1, false>);
-      k<<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr, A.pp_indices,
+      launch_pdl(k, grid, 256, 0, s, A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr, A.pp_indices,
                              A.pp_data, x, b, y);
       return;
     }
     if (idx32) {
       if (mode == 0)
-        spmv32_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+        launch_pdl(spmv32_kernel<NC, 0>, grid, 256, 0, s, A.n_nodes, A.indptr, A.indices, A.data,
                                                   A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
       else
-        spmv32_kernel<NC, 1><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data,
+        launch_pdl(spmv32_kernel<NC, 1>, grid, 256, 0, s, A.n_nodes, A.indptr, A.indices, A.data,
                                                   A.pp_indptr, A.pp_indices, A.pp_data, x, b, y);
       return;
     }
   }
   if (mode == 0)
-    spmv_kernel<NC, 0><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
+    launch_pdl(spmv_kernel<NC, 0>, grid, 256, 0, s, A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
                                             A.pp_indices, A.pp_data, x, b, y);
   else
-    spmv_kernel<NC, 1><<<grid, 256, 0, s>>>(A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
+    launch_pdl(spmv_kernel<NC, 1>, grid, 256, 0, s, A.n_nodes, A.indptr, A.indices, A.data, A.pp_indptr,
                                             A.pp_indices, A.pp_data, x, b, y);
 }
 
@@ -1922,21 +1973,20 @@ void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, 
     const int sgrid = (int)total;
     if constexpr (LD % 4 == 0) {
       if (v4) {
-        vanka_apply_split_kernel<NP, LD, NC, 4, 4>
-            <<<sgrid, ApplyShape<LD, 4>::TPP * 4, 0, s>>>(G, d);
+        launch_pdl(vanka_apply_split_kernel<NP, LD, NC, 4, 4>, sgrid, ApplyShape<LD, 4>::TPP * 4, 0, s, G, d);
         return;
       }
     }
-    vanka_apply_split_kernel<NP, LD, NC, 2, 4><<<sgrid, ApplyShape<LD, 2>::TPP * 4, 0, s>>>(G, d);
+    launch_pdl(vanka_apply_split_kernel<NP, LD, NC, 2, 4>, sgrid, ApplyShape<LD, 2>::TPP * 4, 0, s, G, d);
     return;
   }
   if constexpr (LD % 4 == 0) {
     if (v4) {
-      vanka_apply_kernel<NP, LD, NC, 4><<<grid, ApplyShape<LD, 4>::BLK, 0, s>>>(G, d);
+      launch_pdl(vanka_apply_kernel<NP, LD, NC, 4>, grid, ApplyShape<LD, 4>::BLK, 0, s, G, d);
       return;
     }
   }
-  vanka_apply_kernel<NP, LD, NC, 2><<<grid, ApplyShape<LD, 2>::BLK, 0, s>>>(G, d);
+  launch_pdl(vanka_apply_kernel<NP, LD, NC, 2>, grid, ApplyShape<LD, 2>::BLK, 0, s, G, d);
 }
 
 // batched blocked Gauss-Jordan for the 500 x 500 macro patches (big_* and gj_*
@@ -2069,11 +2119,11 @@ void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int
   if (nc == 4 && n_nodes >= 4 * kSmallLevelNodes &&
       reinterpret_cast<uintptr_t>(Y) % 32 == 0 &&
       reinterpret_cast<uintptr_t>(x) % 32 == 0) {
-    vanka_gather4_kernel<<<grid_for(n_nodes, 256), 256, 0, s>>>(n_nodes, gptr, goff, weight, Y,
+    launch_pdl(vanka_gather4_kernel, grid_for(n_nodes, 256), 256, 0, s, n_nodes, gptr, goff, weight, Y,
                                                                  x, omega, init_zero);
     return;
   }
-  vanka_gather_kernel<<<grid_for(ndof, 256), 256, 0, s>>>(ndof, nc, gptr, goff, weight, Y, x,
+  launch_pdl(vanka_gather_kernel, grid_for(ndof, 256), 256, 0, s, ndof, nc, gptr, goff, weight, Y, x,
                                                            omega, init_zero);
 }
 
@@ -2083,10 +2133,10 @@ void launch_restrict(int64_t n_coarse, int nc, const int64_t* ptr, const int32_t
   // restriction rows are long (a coarse node collects ~100 fine nodes): a
   // thread per (row, component), or 8 lanes per (row, component) on small levels
   if (n_coarse < kSmallLevelNodes)
-    transfer_split_kernel<<<grid_for(n_coarse * nc * 8, 256), 256, 0, s>>>(
+    launch_pdl(transfer_split_kernel, grid_for(n_coarse * nc * 8, 256), 256, 0, s, 
         n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
   else
-    transfer_kernel<<<grid_for(n_coarse * nc, 256), 256, 0, s>>>(
+    launch_pdl(transfer_kernel, grid_for(n_coarse * nc, 256), 256, 0, s, 
         n_coarse, nc, ptr, idx, val, r_fine, constrained_coarse, b_coarse, 0);
 }
 
@@ -2094,10 +2144,10 @@ void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_
                         const double* val, const double* x_coarse,
                         const uint8_t* constrained_fine, double* x_fine, cudaStream_t s) {
   if (nc == 4 && vec4_ok(x_coarse, 0, 4) && vec4_ok(x_fine, 0, 4))
-    transfer4_kernel<<<grid_for(n_fine, 128), 128, 0, s>>>(n_fine, ptr, idx, val, x_coarse,
+    launch_pdl(transfer4_kernel, grid_for(n_fine, 128), 128, 0, s, n_fine, ptr, idx, val, x_coarse,
                                                            constrained_fine, x_fine, 1);
   else
-    transfer_kernel<<<grid_for(n_fine * nc, 256), 256, 0, s>>>(
+    launch_pdl(transfer_kernel, grid_for(n_fine * nc, 256), 256, 0, s, 
         n_fine, nc, ptr, idx, val, x_coarse, constrained_fine, x_fine, 1);
 }
 
@@ -2228,61 +2278,61 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
 
 void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
                          cudaStream_t s) {
-  dense_matvec_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(n, M, x, y);
+  launch_pdl(dense_matvec_kernel, grid_for(n * 32, 256), 256, 0, s, n, M, x, y);
 }
 
 int launch_multi_dot(GmresCtl* ctl, int max_nvec, const double* V, int64_t ldv, const double* w,
                      int64_t n, double* partial, double* out, const int* flag, cudaStream_t s) {
   if (vec4_ok(V, ldv, n) && vec4_ok(w, 0, n))
-    multi_dot_kernel<4><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, w, n, partial, flag);
+    launch_pdl(multi_dot_kernel<4>, kRedBlocks, 256, 0, s, ctl, V, ldv, w, n, partial, flag);
   else
-    multi_dot_kernel<1><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, w, n, partial, flag);
-  reduce_partials_kernel<<<max_nvec + 1, 256, 0, s>>>(0, kRedBlocks, partial, out, flag, ctl);
+    launch_pdl(multi_dot_kernel<1>, kRedBlocks, 256, 0, s, ctl, V, ldv, w, n, partial, flag);
+  launch_pdl(reduce_partials_kernel, max_nvec + 1, 256, 0, s, 0, kRedBlocks, partial, out, flag, ctl);
   return 2;
 }
 
 int launch_multi_axpy(GmresCtl* ctl, const double* V, int64_t ldv, const double* h, double* w,
                       int64_t n, double* partial, double* out, const int* flag, cudaStream_t s) {
   if (vec4_ok(V, ldv, n) && vec4_ok(w, 0, n))
-    multi_axpy_kernel<4><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, h, w, n, partial, flag);
+    launch_pdl(multi_axpy_kernel<4>, kRedBlocks, 256, 0, s, ctl, V, ldv, h, w, n, partial, flag);
   else
-    multi_axpy_kernel<1><<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, h, w, n, partial, flag);
-  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, out, flag, nullptr);
+    launch_pdl(multi_axpy_kernel<1>, kRedBlocks, 256, 0, s, ctl, V, ldv, h, w, n, partial, flag);
+  launch_pdl(reduce_partials_kernel, 1, 256, 0, s, 1, kRedBlocks, partial, out, flag, nullptr);
   return 2;
 }
 
 int launch_arnoldi_finish(GmresCtl* ctl, double* hcol, double* h2, const double* na2, int stage,
                           cudaStream_t s) {
-  arnoldi_finish_kernel<<<1, 256, 0, s>>>(ctl, hcol, h2, na2, stage);
+  launch_pdl(arnoldi_finish_kernel, 1, 256, 0, s, ctl, hcol, h2, na2, stage);
   return 1;
 }
 
 int launch_scale_copy_slot(const GmresCtl* ctl, const double* w, double* V, int64_t ldv,
                            const double* hcol, double* vin, int64_t n, cudaStream_t s) {
-  scale_copy_slot_kernel<<<kRedBlocks, 256, 0, s>>>(ctl, w, V, ldv, hcol, vin, n);
+  launch_pdl(scale_copy_slot_kernel, kRedBlocks, 256, 0, s, ctl, w, V, ldv, hcol, vin, n);
   return 1;
 }
 
 int launch_gmres_init(GmresCtl* ctl, const double* b, int64_t n, double* partial, double* scal,
                       double* res, double* g, double* v0, double* vin,
                       cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
-  sumsq_kernel<<<kRedBlocks, 256, 0, s>>>(b, n, partial);
-  reduce_partials_kernel<<<1, 256, 0, s>>>(1, kRedBlocks, partial, scal, nullptr, nullptr);
-  gmres_init_kernel<<<1, 1, 0, s>>>(ctl, scal, res, g, cond, use_cond);
-  scale_dual_kernel<<<kRedBlocks, 256, 0, s>>>(ctl, b, v0, vin, n);
+  launch_pdl(sumsq_kernel, kRedBlocks, 256, 0, s, b, n, partial);
+  launch_pdl(reduce_partials_kernel, 1, 256, 0, s, 1, kRedBlocks, partial, scal, nullptr, nullptr);
+  launch_pdl(gmres_init_kernel, 1, 1, 0, s, ctl, scal, res, g, cond, use_cond);
+  launch_pdl(scale_dual_kernel, kRedBlocks, 256, 0, s, ctl, b, v0, vin, n);
   return 4;
 }
 
 int launch_givens(GmresCtl* ctl, const double* hcol, double* H, double* cs, double* sn, double* g,
                   double* res, cudaGraphConditionalHandle cond, int use_cond, cudaStream_t s) {
-  givens_kernel<<<1, 1, 0, s>>>(ctl, hcol, H, cs, sn, g, res, cond, use_cond);
+  launch_pdl(givens_kernel, 1, 1, 0, s, ctl, hcol, H, cs, sn, g, res, cond, use_cond);
   return 1;
 }
 
 int launch_gmres_solution(const GmresCtl* ctl, const double* H, const double* g, double* y,
                           const double* V, int64_t ldv, double* out, int64_t n, cudaStream_t s) {
-  backsolve_kernel<<<1, 1, 0, s>>>(ctl, H, g, y);
-  combine_kernel<<<kRedBlocks, 256, 0, s>>>(ctl, V, ldv, y, out, n);
+  launch_pdl(backsolve_kernel, 1, 1, 0, s, ctl, H, g, y);
+  launch_pdl(combine_kernel, kRedBlocks, 256, 0, s, ctl, V, ldv, y, out, n);
   return 2;
 }
 

@@ -1,4 +1,4 @@
-"""Coarse-level inverse A/B on the GPU box (ALEFSI_GJ_BLOCKED=0|1).
+"""Coarse-level inverse check on the GPU box.
 
     python scripts/coarse_ab.py [workload]
 
@@ -38,7 +38,7 @@ def main():
     r = mg.spmv(0, y, x)          # x - A0 y
     torch.cuda.synchronize()
     sol, st = mg.gmres(b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
-    print(json.dumps({"workload": name, "blocked": os.environ.get("ALEFSI_GJ_BLOCKED", "1"),
+    print(json.dumps({"workload": name,
                       "coarse_dofs": n0, "factorize_s": ts,
                       "coarse_rel_residual": float(torch.linalg.norm(r) / torch.linalg.norm(x)),
                       "y_head": y[:4].cpu().tolist(), "its": st.iterations,

@@ -1,5 +1,5 @@
-"""Vanka + coarse factorisation A/B on the GPU box (ALEFSI_FACT_TAIL,
-ALEFSI_GJ_CLUSTER, ALEFSI_GJ_BLOCKED switches).
+"""Vanka + coarse factorisation timing on the GPU box (the A/B switches of
+round 1 are gone from the library; DESIGN.md keeps their measurements).
 
     python scripts/fact_ab.py [workload ...]
 
@@ -35,8 +35,7 @@ def main():
         sol, st = mg.gmres(b, rel_tol=wl.rel_tol, max_iter=getattr(wl, "max_iter", 250))
         h = hashlib.sha256((sol.cpu().numpy() if hasattr(sol, "cpu") else np.asarray(sol)).tobytes()).hexdigest()[:16]
         hh = hashlib.sha256(np.asarray(st.residuals).tobytes()).hexdigest()[:16]
-        env = {k: v for k, v in os.environ.items() if k.startswith("ALEFSI_")}
-        print(json.dumps({"workload": name, "env": env,
+        print(json.dumps({"workload": name,
                           "factorize_s": ts, "its": st.iterations, "hash_x": h,
                           "hash_history": hh}), flush=True)
         del mg, prob

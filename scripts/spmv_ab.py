@@ -1,6 +1,6 @@
-"""SpMV A/B on the GPU box: hash and time every level's operator product.
+"""Per-level SpMV on the GPU box: hash and time every level's operator product.
 
-    ALEFSI_SPMV_TMA=0|1 python scripts/spmv_ab.py [workload] [--reps N]
+    python scripts/spmv_ab.py [workload] [--reps N]
 
 Prints one JSON line per level: SHA-256 of y = A x and of y = b - A x for a
 seeded x (bitwise comparison across kernel variants) and the mean CUDA-event
@@ -51,8 +51,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
-        print(json.dumps({"workload": name, "level": l, "tma": os.environ.get("ALEFSI_SPMV_TMA", "1"),
-                          "nodes": p.n_nodes, "hash_Ax": h0, "hash_b_Ax": h1, "ms": ms,
+        print(json.dumps({"workload": name, "level": l, "nodes": p.n_nodes, "hash_Ax": h0, "hash_b_Ax": h1, "ms": ms,
                           "GBs": alg / ms / 1e6}), flush=True)
 
 
