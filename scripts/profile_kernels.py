@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
-from paper_1904_02401_b200 import device, workloads as W  # noqa: E402
+from paper_1904_02401_b200 import workloads as W  # noqa: E402
 
 
 def main():
@@ -22,9 +22,8 @@ def main():
     standalone = "--standalone" in sys.argv
     wl = W.CONFIGS[name]
     t = time.time()
-    case = W.build_case(wl, with_coloring=False)
-    solver = device.DeviceMgSolver.from_case(case, wl)
-    b = torch.from_numpy(case.b).cuda()
+    prob, solver, bh, _ = W.build_device_solver(wl)      # the bench.py path
+    b = torch.from_numpy(bh).cuda()
     torch.cuda.synchronize()
     print(f"setup {time.time() - t:.1f}s", flush=True)
     L = solver.n_levels - 1
