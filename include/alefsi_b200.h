@@ -207,6 +207,13 @@ int alefsi_mg_apply(alefsi_mg h, const double* b, double* z, int32_t host_ptrs);
 /* y = A x (b == NULL) or y = b - A x on one level (DEVICE). */
 int alefsi_mg_spmv(alefsi_mg h, int32_t level, const double* x, const double* b, double* y);
 
+/* Layout of a 2D (nc = 3) level's SpMV copy: sliced ELL with lanes_per_row
+ * = 1, 2 or 4 lanes per block row (slices of 32 / lanes rows), or 0 for the
+ * CSR half-warp kernel.  The default is chosen by level size at
+ * set_pattern / set_matrix; this call re-lays a level out (tuning,
+ * measurements).  No effect on other nc. */
+int alefsi_mg_set_sell(alefsi_mg h, int32_t level, int32_t lanes_per_row);
+
 /* x <- one damped additive Vanka sweep (VankaSmoother.sweep,
  * reference linsolve.py:167-178) (DEVICE). */
 int alefsi_mg_vanka_sweep(alefsi_mg h, int32_t level, double* x, const double* b);

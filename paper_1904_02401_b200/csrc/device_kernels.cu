@@ -347,13 +347,15 @@ __global__ void __launch_bounds__(256) spmv_half_kernel(int64_t n, const int64_t
   }
 }
 
-// 2D (NC = 3) operator in sliced-ELL form: warp = 32 consecutive block rows,
-// lane = row.  Every element of a slot is one coalesced 256-byte warp load
-// (evict-first), the column index one 128-byte load; the x block is read
-// through the read-only path (x stays L2-resident).  A row sums its blocks
-// in pattern order, then its pressure-extension entries.  Padding slots hold
-// zeros and a valid column.
-template <int MODE>
+// 2D (NC = 3) operator in sliced-ELL form: warp = one slice of R = 32 / T
+// consecutive block rows, T lanes per row taking the row's slots round-robin
+// (T = 1: lane = row, slots in pattern order).  Every element plane of a
+// slot is one coalesced R*8-byte segment (a warp load covers T consecutive
+// slots, evict-first), the columns an R*4-byte segment; x is read through
+// the read-only path (x stays L2-resident).  A lane sums its slots in order,
+// its row's pressure-extension entries likewise; the T partial sums are
+// combined by xor-shuffles.  Padding slots hold zeros and a valid column.
+template <int MODE, int T>
 __global__ void __launch_bounds__(256) spmv3_sell_kernel(int64_t n, int64_t n_slices,
                                                          const int64_t* __restrict__ off,
                                                          const int32_t* __restrict__ col,
@@ -365,20 +367,20 @@ __global__ void __launch_bounds__(256) spmv3_sell_kernel(int64_t n, int64_t n_sl
                                                          const double* __restrict__ b,
                                                          double* __restrict__ y) {
   pdl_entry();
-  constexpr int NC = 3;
-  const int lane = threadIdx.x & 31;
+  constexpr int NC = 3, R = 32 / T;
+  const int lane = threadIdx.x & 31, q = lane % R, h = lane / R;
   const int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (sl >= n_slices) return;
-  const int64_t row = sl * 32 + lane;
+  const int64_t row = sl * R + q;
   const int64_t g0 = off[sl], g1 = off[sl + 1];
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll 2
-  for (int64_t g = g0; g < g1; ++g) {
-    const int c = __ldcs(col + g * 32 + lane);
-    const double* v = val + g * (NC * NC * 32) + lane;
+  for (int64_t g = g0 + h; g < g1; g += T) {
+    const int c = __ldcs(col + g * R + q);
+    const double* v = val + g * (NC * NC * R) + q;
     double e[NC * NC];
 #pragma unroll
-    for (int q = 0; q < NC * NC; ++q) e[q] = __ldcs(v + q * 32);
+    for (int k = 0; k < NC * NC; ++k) e[k] = __ldcs(v + k * R);
     const double x0 = __ldg(x + (int64_t)c * NC), x1 = __ldg(x + (int64_t)c * NC + 1),
                  x2 = __ldg(x + (int64_t)c * NC + 2);
     a0 = fma(e[0], x0, a0); a0 = fma(e[1], x1, a0); a0 = fma(e[2], x2, a0);
@@ -389,11 +391,17 @@ __global__ void __launch_bounds__(256) spmv3_sell_kernel(int64_t n, int64_t n_sl
     double ap = 0.0;
     const int64_t p0 = poff[sl], p1 = poff[sl + 1];
 #pragma unroll 4
-    for (int64_t g = p0; g < p1; ++g)
-      ap = fma(__ldcs(pval + g * 32 + lane), __ldg(x + (int64_t)__ldcs(pcol + g * 32 + lane) * NC), ap);
+    for (int64_t g = p0 + h; g < p1; g += T)
+      ap = fma(__ldcs(pval + g * R + q), __ldg(x + (int64_t)__ldcs(pcol + g * R + q) * NC), ap);
     a0 += ap;
   }
-  if (row >= n) return;
+#pragma unroll
+  for (int o = R; o < 32; o <<= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+  }
+  if (h != 0 || row >= n) return;
   const int64_t o = row * NC;
   if (MODE == 1) {
     y[o] = b[o] - a0;
@@ -406,14 +414,14 @@ __global__ void __launch_bounds__(256) spmv3_sell_kernel(int64_t n, int64_t n_sl
   }
 }
 
-__global__ void sell_pack_kernel(int64_t n_pos, int nc2, const int64_t* __restrict__ map,
+__global__ void sell_pack_kernel(int64_t n_pos, int R, int nc2, const int64_t* __restrict__ map,
                                  const double* __restrict__ data, double* __restrict__ val) {
   for (int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < n_pos;
        pos += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = map[pos];
-    const int64_t g = pos >> 5, lane = pos & 31;
-    double* out = val + g * nc2 * 32 + lane;
-    for (int q = 0; q < nc2; ++q) out[q * 32] = m >= 0 ? data[m * nc2 + q] : 0.0;
+    const int64_t g = pos / R, q = pos - g * R;
+    double* out = val + g * nc2 * R + q;
+    for (int k = 0; k < nc2; ++k) out[k * R] = m >= 0 ? data[m * nc2 + k] : 0.0;
   }
 }
 
@@ -1895,14 +1903,11 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
   if constexpr (NC == 3) {
     if (A.sell_off != nullptr) {
       const int sgrid = grid_for(A.n_slices * 32, 256);
-      if (mode == 0)
-        launch_pdl(spmv3_sell_kernel<0>, sgrid, 256, 0, s, A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
-                                                   A.sell_val, A.sell_poff, A.sell_pcol,
-                                                   A.sell_pval, x, b, y);
-      else
-        launch_pdl(spmv3_sell_kernel<1>, sgrid, 256, 0, s, A.n_nodes, A.n_slices, A.sell_off, A.sell_col,
-                                                   A.sell_val, A.sell_poff, A.sell_pcol,
-                                                   A.sell_pval, x, b, y);
+      auto k = A.sell_lanes == 4 ? (mode == 0 ? spmv3_sell_kernel<0, 4> : spmv3_sell_kernel<1, 4>)
+             : A.sell_lanes == 2 ? (mode == 0 ? spmv3_sell_kernel<0, 2> : spmv3_sell_kernel<1, 2>)
+                                 : (mode == 0 ? spmv3_sell_kernel<0, 1> : spmv3_sell_kernel<1, 1>);
+      launch_pdl(k, sgrid, 256, 0, s, A.n_nodes, A.n_slices, A.sell_off, A.sell_col, A.sell_val,
+                 A.sell_poff, A.sell_pcol, A.sell_pval, x, b, y);
       return;
     }
     const int hgrid = grid_for(A.n_nodes * 16, 256);
@@ -2045,11 +2050,11 @@ void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y
   else if (A.nc == 2) spmv_dispatch<2>(A, x, b, y, mode, s);
 }
 
-void launch_sell_pack(int64_t n_pos, int nc2, const int64_t* map, const double* data, double* val,
-                      cudaStream_t s) {
+void launch_sell_pack(int64_t n_pos, int R, int nc2, const int64_t* map, const double* data,
+                      double* val, cudaStream_t s) {
   if (n_pos == 0) return;
   sell_pack_kernel<<<(int)std::min<int64_t>(grid_for(n_pos, 256), 4 * 148 * 8), 256, 0, s>>>(
-      n_pos, nc2, map, data, val);
+      n_pos, R, nc2, map, data, val);
 }
 
 int64_t vanka_factorize_work(int np, int64_t n_patches) {

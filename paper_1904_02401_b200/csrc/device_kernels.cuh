@@ -15,13 +15,16 @@ struct DevMatrix {
   const int64_t* pp_indptr = nullptr;
   const int32_t* pp_indices = nullptr;
   const double* pp_data = nullptr;
-  // optional sliced-ELL copy used by the SpMV (nc == 3): slices of 32
+  // optional sliced-ELL copy used by the SpMV (nc == 3): slices of R
   // consecutive block rows, slice s holds its rows' k-th blocks in slot
-  // off[s] + k, a slot = nc*nc element planes of 32 doubles (one per row)
+  // off[s] + k, a slot = nc*nc element planes of R doubles (one per row)
+  // (R = 32 / sell_lanes rows per slice; a row's slots are split
+  // round-robin over its sell_lanes lanes)
   int64_t n_slices = 0;
+  int sell_lanes = 0;
   const int64_t* sell_off = nullptr;    // n_slices + 1 (slot units)
-  const int32_t* sell_col = nullptr;    // slots * 32 block columns
-  const double* sell_val = nullptr;     // slots * nc*nc * 32
+  const int32_t* sell_col = nullptr;    // slots * R block columns
+  const double* sell_val = nullptr;     // slots * nc*nc * R
   const int64_t* sell_poff = nullptr;   // pressure extension, same scheme (nullptr: none)
   const int32_t* sell_pcol = nullptr;
   const double* sell_pval = nullptr;
@@ -29,8 +32,8 @@ struct DevMatrix {
 
 // refresh the sliced-ELL values from the CSR data: map[pos] = CSR block (or
 // entry) index of slot position pos, -1 for padding (stored as zero)
-void launch_sell_pack(int64_t n_pos, int nc2, const int64_t* map, const double* data, double* val,
-                      cudaStream_t s);
+void launch_sell_pack(int64_t n_pos, int R, int nc2, const int64_t* map, const double* data,
+                      double* val, cudaStream_t s);
 
 // y = A x (mode 0) or y = b - A x (mode 1)
 void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y, int mode,

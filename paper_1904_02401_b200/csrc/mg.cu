@@ -161,6 +161,7 @@ struct Level {
 
   // sliced-ELL copy of the operator for the SpMV (nc == 3), see DevMatrix
   int64_t n_slices = 0, sell_slots = 0, sell_pslots = 0;
+  int sell_lanes = 0;     // lanes per row (slice height 32 / lanes); 0: none
   bool sell_dirty = false;
   DevBuf<int64_t> sell_off, sell_poff, sell_map, sell_pmap;
   DevBuf<int32_t> sell_col, sell_pcol;
@@ -181,6 +182,7 @@ struct Level {
     m.pp_data = pp_data.p;
     if (n_slices > 0) {
       m.n_slices = n_slices;
+      m.sell_lanes = sell_lanes;
       m.sell_off = sell_off.p;
       m.sell_col = sell_col.p;
       m.sell_val = sell_val.p;
@@ -194,28 +196,39 @@ struct Level {
   }
 };
 
-constexpr int64_t kSellMinNodes = 1 << 18;
+// Lanes per block row of the sliced-ELL SpMV by level size (0: the
+// half-warp CSR kernel).  Measured on config 1 (scripts/spmv_ab.py,
+// DESIGN.md): one lane per row needs >= ~2^20 rows to hide the serial walk
+// over a row's blocks; smaller levels split a row over 2 or 4 lanes.
+int default_sell_lanes(int nc, int64_t n_nodes) {
+  if (nc != 3) return 0;
+  if (n_nodes >= (int64_t)1 << 20) return 1;
+  if (n_nodes >= (int64_t)1 << 18) return 2;
+  if (n_nodes >= (int64_t)1 << 16) return 4;
+  return 0;
+}
 
-// Sliced-ELL index of a CSR pattern (32-row slices, no row permutation: the
-// Q2 node numbering keeps rows of one slice at nearly equal length — config 1
-// finest level: 0.25 % block padding).  pos = slot * 32 + lane.
-void sell_index(int64_t n, const int64_t* ptr, const int32_t* idx, std::vector<int64_t>& off,
+// Sliced-ELL index of a CSR pattern: slices of R = 32 / lanes consecutive
+// rows, no row permutation (the Q2 node numbering keeps the rows of a slice
+// at nearly equal length — config 1 finest level: 0.25 % block padding).
+// pos = slot * R + row-in-slice.
+void sell_index(int64_t n, int R, const int64_t* ptr, const int32_t* idx, std::vector<int64_t>& off,
                 std::vector<int32_t>& col, std::vector<int64_t>& map) {
-  const int64_t ns = (n + 31) / 32;
+  const int64_t ns = (n + R - 1) / R;
   off.assign(ns + 1, 0);
   for (int64_t sl = 0; sl < ns; ++sl) {
     int64_t w = 0;
-    for (int64_t r = sl * 32; r < std::min(n, sl * 32 + 32); ++r) w = std::max(w, ptr[r + 1] - ptr[r]);
+    for (int64_t r = sl * R; r < std::min(n, sl * R + R); ++r) w = std::max(w, ptr[r + 1] - ptr[r]);
     off[sl + 1] = off[sl] + w;
   }
-  col.assign((size_t)off[ns] * 32, 0);
-  map.assign((size_t)off[ns] * 32, -1);
+  col.assign((size_t)off[ns] * R, 0);
+  map.assign((size_t)off[ns] * R, -1);
   for (int64_t sl = 0; sl < ns; ++sl)
-    for (int lane = 0; lane < 32; ++lane) {
-      const int64_t r = sl * 32 + lane;
+    for (int q = 0; q < R; ++q) {
+      const int64_t r = sl * R + q;
       const int64_t len = r < n ? ptr[r + 1] - ptr[r] : 0;
       for (int64_t k = 0; k < off[sl + 1] - off[sl]; ++k) {
-        const size_t pos = (size_t)(off[sl] + k) * 32 + lane;
+        const size_t pos = (size_t)(off[sl] + k) * R + q;
         // padding: zero value on a valid column (the row itself, else 0)
         col[pos] = k < len ? idx[ptr[r] + k] : (int32_t)(r < n ? r : 0);
         map[pos] = k < len ? ptr[r] + k : -1;
@@ -223,35 +236,37 @@ void sell_index(int64_t n, const int64_t* ptr, const int32_t* idx, std::vector<i
     }
 }
 
-int build_sell(Level& L, const int64_t* indptr, const int32_t* indices, const int64_t* pp_indptr,
-               const int32_t* pp_indices, cudaStream_t s) {
+int build_sell(Level& L, int lanes, const int64_t* indptr, const int32_t* indices,
+               const int64_t* pp_indptr, const int32_t* pp_indices, cudaStream_t s) {
   L.n_slices = 0;
+  L.sell_lanes = 0;
   L.sell_slots = L.sell_pslots = 0;
-  // large levels only: a lane walks its row's blocks serially, which the
-  // small, L2-resident levels cannot hide (2d_large level 3, 66k nodes:
-  // 76 us with sliced ELL); they keep the half-warp-per-row kernel
-  if (L.nc != 3 || L.n_nodes < kSellMinNodes) return ALEFSI_OK;
+  if (L.nc != 3 || L.n_nodes == 0 || lanes == 0) return ALEFSI_OK;
+  if (lanes != 1 && lanes != 2 && lanes != 4)
+    return fail(ALEFSI_ERR_ARG, "sliced ELL: 1, 2 or 4 lanes per row");
+  const int R = 32 / lanes;
   std::vector<int64_t> off, map;
   std::vector<int32_t> col;
-  sell_index(L.n_nodes, indptr, indices, off, col, map);
+  sell_index(L.n_nodes, R, indptr, indices, off, col, map);
   const int64_t ns = (int64_t)off.size() - 1;
   CK(L.sell_off.upload(off.data(), off.size(), s));
   CK(L.sell_col.upload(col.data(), col.size(), s));
   CK(L.sell_map.upload(map.data(), map.size(), s));
-  CK(L.sell_val.ensure((size_t)off[ns] * 32 * 9));
+  CK(L.sell_val.ensure((size_t)off[ns] * R * 9));
   L.sell_slots = off[ns];
   if (L.nnz_pp > 0) {
     std::vector<int64_t> poff, pmap;
     std::vector<int32_t> pcol;
-    sell_index(L.n_nodes, pp_indptr, pp_indices, poff, pcol, pmap);
+    sell_index(L.n_nodes, R, pp_indptr, pp_indices, poff, pcol, pmap);
     CK(L.sell_poff.upload(poff.data(), poff.size(), s));
     CK(L.sell_pcol.upload(pcol.data(), pcol.size(), s));
     CK(L.sell_pmap.upload(pmap.data(), pmap.size(), s));
-    CK(L.sell_pval.ensure((size_t)poff[ns] * 32));
+    CK(L.sell_pval.ensure((size_t)poff[ns] * R));
     L.sell_pslots = poff[ns];
   }
   CK(cudaStreamSynchronize(s));     // host index vectors go out of scope
   L.n_slices = ns;
+  L.sell_lanes = lanes;
   L.sell_dirty = true;
   return ALEFSI_OK;
 }
@@ -259,9 +274,10 @@ int build_sell(Level& L, const int64_t* indptr, const int32_t* indices, const in
 // refresh the sliced-ELL values after the CSR data changed
 void refresh_sell(Level& L, cudaStream_t s) {
   if (L.n_slices == 0 || !L.sell_dirty) return;
-  launch_sell_pack(L.sell_slots * 32, 9, L.sell_map.p, L.data.p, L.sell_val.p, s);
+  const int R = 32 / L.sell_lanes;
+  launch_sell_pack(L.sell_slots * R, R, 9, L.sell_map.p, L.data.p, L.sell_val.p, s);
   if (L.sell_pslots > 0)
-    launch_sell_pack(L.sell_pslots * 32, 1, L.sell_pmap.p, L.pp_data.p, L.sell_pval.p, s);
+    launch_sell_pack(L.sell_pslots * R, R, 1, L.sell_pmap.p, L.pp_data.p, L.sell_pval.p, s);
   L.sell_dirty = false;
 }
 
@@ -926,7 +942,8 @@ int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nn
     CKAPI(L.pp_data.upload(pp_data, nnz_pp, m->stream));
   }
   L.nc = nc;
-  rc = alefsi::build_sell(L, indptr, indices, pp_indptr, pp_indices, m->stream);
+  rc = alefsi::build_sell(L, alefsi::default_sell_lanes(nc, n_nodes), indptr, indices, pp_indptr,
+                         pp_indices, m->stream);
   if (rc) return rc;
   if (level == 0) {
     const int64_t n0 = n_nodes * nc;
@@ -979,7 +996,8 @@ int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t n
     CKAPI(cudaMemsetAsync(L.pp_data.p, 0, sizeof(double) * nnz_pp, m->stream));
   }
   L.nc = nc;
-  rc = alefsi::build_sell(L, indptr, indices, pp_indptr, pp_indices, m->stream);
+  rc = alefsi::build_sell(L, alefsi::default_sell_lanes(nc, n_nodes), indptr, indices, pp_indptr,
+                         pp_indices, m->stream);
   if (rc) return rc;
   L.host_dense.clear();
   CKAPI(cudaStreamSynchronize(m->stream));
@@ -1440,6 +1458,33 @@ int alefsi_mg_apply(alefsi_mg h, const double* b, double* z, int32_t host_ptrs) 
   if (rc) return rc;
   CKAPI(cudaMemcpyAsync(z, m->xb.p, sizeof(double) * n, cudaMemcpyDeviceToHost, m->stream));
   CKAPI(cudaStreamSynchronize(m->stream));
+  return ALEFSI_OK;
+  ALEFSI_TRY_END
+}
+
+int alefsi_mg_set_sell(alefsi_mg h, int32_t level, int32_t lanes_per_row) {
+  ALEFSI_TRY_BEGIN
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  auto& L = m->lv[level];
+  if (!L.has_matrix) return fail(ALEFSI_ERR_STATE, "set_sell before the level's pattern");
+  std::vector<int64_t> ip(L.n_nodes + 1), pp;
+  std::vector<int32_t> ix(L.nnzb), px;
+  CKAPI(cudaMemcpy(ip.data(), L.indptr.p, sizeof(int64_t) * ip.size(), cudaMemcpyDeviceToHost));
+  CKAPI(cudaMemcpy(ix.data(), L.indices.p, sizeof(int32_t) * ix.size(), cudaMemcpyDeviceToHost));
+  if (L.nnz_pp > 0) {
+    pp.resize(L.n_nodes + 1);
+    px.resize(L.nnz_pp);
+    CKAPI(cudaMemcpy(pp.data(), L.pp_indptr.p, sizeof(int64_t) * pp.size(), cudaMemcpyDeviceToHost));
+    CKAPI(cudaMemcpy(px.data(), L.pp_indices.p, sizeof(int32_t) * px.size(), cudaMemcpyDeviceToHost));
+  }
+  rc = alefsi::build_sell(L, lanes_per_row, ip.data(), ix.data(), pp.data(), px.data(), m->stream);
+  if (rc) return rc;
+  alefsi::refresh_sell(L, m->stream);
+  CKAPI(cudaStreamSynchronize(m->stream));
+  m->graph_valid = false;
+  m->solve_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }

@@ -237,6 +237,11 @@ class DeviceMgSolver:
         _lib.call("alefsi_mg_spmv", self._h, level, x, b if b is not None else None, y)
         return y
 
+    def set_sell(self, level, lanes_per_row):
+        """Re-lay a 2D level's SpMV copy out as sliced ELL with 1, 2 or 4
+        lanes per row (0: CSR half-warp kernel); see alefsi_mg_set_sell."""
+        _lib.call("alefsi_mg_set_sell", self._h, level, int(lanes_per_row))
+
     def sweep(self, level, x, b):
         self._bind_torch_stream()
         _lib.call("alefsi_mg_vanka_sweep", self._h, level, x, b)
