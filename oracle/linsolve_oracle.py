@@ -199,7 +199,10 @@ class MgOracle:
     """V-cycle with Vanka smoothing and a sparse-LU coarse solve
     (linsolve.py:229-270)."""
 
-    def __init__(self, case=None, nu_pre=2, nu_post=2, omega=0.8, threads=1, levels=None):
+    def __init__(self, case=None, nu_pre=2, nu_post=2, omega=0.8, threads=1, levels=None,
+                 inverses=None):
+        """``inverses`` (optional): per level >= 1 the list of patch-group
+        inverses to use instead of factorising (timing samples)."""
         self.nu_pre, self.nu_post = nu_pre, nu_post
         levels = levels if levels is not None else case.mg_levels()
         mats = [lv["matrix"] for lv in levels]
@@ -210,7 +213,10 @@ class MgOracle:
         self.smoothers = [None]
         for l in range(1, len(self.A)):
             sm = VankaOracle(levels[l]["patches"], omega, threads)
-            sm.factorize(mats[l])
+            if inverses is not None:
+                sm.inverses = inverses[l]
+            else:
+                sm.factorize(mats[l])
             self.smoothers.append(sm)
         self.coarse_lu = spla.splu(sp.csc_matrix(mats[0].to_csr()))
 

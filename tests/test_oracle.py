@@ -121,3 +121,14 @@ def test_oracle_vs_live_reference_sweep_weights():
     sm = orc.VankaOracle(case.patches[-1], wl.omega)
     for a, b in zip(sm.weights, sm_ref.weights):
         np.testing.assert_array_equal(a, b)
+
+
+def test_oracle_accepts_precomputed_patch_inverses():
+    """bench.py's cpu_baseline feeds the device's patch inverses to the oracle
+    V-cycle instead of refactorising on the CPU: same V-cycle."""
+    from conftest import get_case
+    case = get_case("2d_mini")
+    mg1 = orc.MgOracle(case)
+    inv = [None] + [sm.inverses for sm in mg1.smoothers[1:]]
+    mg2 = orc.MgOracle(case, inverses=inv)
+    np.testing.assert_array_equal(mg1.dot(case.b), mg2.dot(case.b))
