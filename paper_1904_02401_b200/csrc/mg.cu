@@ -197,14 +197,14 @@ struct Level {
 };
 
 // Lanes per block row of the sliced-ELL SpMV by level size (0: the
-// half-warp CSR kernel).  Measured on config 1 (scripts/spmv_ab.py,
-// DESIGN.md): one lane per row needs >= ~2^20 rows to hide the serial walk
-// over a row's blocks; smaller levels split a row over 2 or 4 lanes.
+// half-warp CSR kernel).  Measured per level of configs 0 and 1
+// (scripts/spmv_layout.py, profiles/r2f_spmv_layout.log): 1,051,137 nodes
+// lanes 1: 247 us (CSR 369); 263,425 nodes lanes 2: 61 us (lanes 1: 107,
+// CSR 87); 66,177 nodes and below the CSR kernel is fastest (25 us vs 26).
 int default_sell_lanes(int nc, int64_t n_nodes) {
   if (nc != 3) return 0;
   if (n_nodes >= (int64_t)1 << 20) return 1;
-  if (n_nodes >= (int64_t)1 << 18) return 2;
-  if (n_nodes >= (int64_t)1 << 16) return 4;
+  if (n_nodes >= (int64_t)1 << 17) return 2;
   return 0;
 }
 

@@ -333,3 +333,29 @@ def test_sliced_ell_layouts_vs_oracle(name):
         assert_history(st, g["residuals"], g["iterations"])
     finally:
         s.close()
+
+
+@pytest.mark.parametrize("name", ["2d_mini", "3d_tiny"])
+def test_graph_solve_edge_cases_match_host_stepped(name):
+    """The one-graph-per-solve GMRES (conditional while node) and the
+    host-stepped loop run the same kernels: identical results for a
+    converged solve, a solve stopped by max_iter (SolverError with the same
+    partial history) and a zero right-hand side (x = 0, no iteration)."""
+    case = get_case(name)
+    wl = W.CONFIGS[name]
+    sg = solver_for(name, use_graph=True)
+    sh = solver_for(name)
+    xg, stg = sg.gmres(case.b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    xh, sth = sh.gmres(case.b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    np.testing.assert_array_equal(xg, xh)
+    assert stg.residuals == sth.residuals
+    for s in (sg, sh):
+        with pytest.raises(device.SolverError) as exc:
+            s.gmres(case.b, rel_tol=1e-14, max_iter=3)
+        assert exc.value.stats.iterations == 3 and not exc.value.stats.converged
+        assert exc.value.stats.residuals == sth.residuals[:4]
+        x0, st0 = s.gmres(np.zeros_like(case.b), rel_tol=1e-8)
+        assert st0.iterations == 0 and not x0.any()
+    # back to a full solve after the early stops: same result again
+    xg2, stg2 = sg.gmres(case.b, rel_tol=wl.rel_tol, max_iter=wl.max_iter)
+    np.testing.assert_array_equal(xg2, xg)
