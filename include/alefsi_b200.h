@@ -214,6 +214,12 @@ int alefsi_mg_spmv(alefsi_mg h, int32_t level, const double* x, const double* b,
  * measurements).  No effect on other nc. */
 int alefsi_mg_set_sell(alefsi_mg h, int32_t level, int32_t lanes_per_row);
 
+/* Form of a level's Vanka apply kernel: -1 (default) column-split patches
+ * (4 thread groups per patch, partials combined in fixed order) for launches
+ * of fewer than 8,192 patches, one thread group per patch otherwise; 0 / 1
+ * force the unsplit / split form (tuning, measurements; patches <= 108 dofs). */
+int alefsi_mg_set_apply_split(alefsi_mg h, int32_t level, int32_t split);
+
 /* x <- one damped additive Vanka sweep (VankaSmoother.sweep,
  * reference linsolve.py:167-178) (DEVICE). */
 int alefsi_mg_vanka_sweep(alefsi_mg h, int32_t level, double* x, const double* b);

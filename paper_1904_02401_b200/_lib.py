@@ -43,6 +43,7 @@ SIGNATURES = {
     "alefsi_mg_apply": [_p, _p, _p, _i32],
     "alefsi_mg_spmv": [_p, _i32, _p, _p, _p],
     "alefsi_mg_set_sell": [_p, _i32, _i32],
+    "alefsi_mg_set_apply_split": [_p, _i32, _i32],
     "alefsi_mg_vanka_sweep": [_p, _i32, _p, _p],
     "alefsi_mg_restrict": [_p, _i32, _p, _p],
     "alefsi_mg_prolong_add": [_p, _i32, _p, _p],

@@ -1949,7 +1949,8 @@ void spmv_dispatch(const DevMatrix& A, const double* x, const double* b, double*
 }
 
 template <int NP, int LD, int NC>
-void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, cudaStream_t s) {
+void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, int split,
+                    cudaStream_t s) {
   bool v4 = false;
   if constexpr (LD % 4 == 0) {
     v4 = true;
@@ -1972,7 +1973,10 @@ void apply_dispatch(const DevPatchGroup* g, int ng, const double* d, double* Y, 
   }
   if (grid == 0) return;
   const int64_t total = G.n_patches[0] + G.n_patches[1];
-  if (total < kSmallPatchCount && NP <= 108) {
+  // column-split form: by default for launches of < kSmallPatchCount patches
+  // (L2-resident levels); split = 0 / 1 forces the choice (tuning)
+  const bool use_split = NP <= 108 && (split < 0 ? total < kSmallPatchCount : split > 0);
+  if (use_split) {
     // one CTA per patch, 4 column splits
     G.blocks0 = (int)G.n_patches[0];
     const int sgrid = (int)total;
@@ -2093,7 +2097,7 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
 // one launch per pair of consecutive groups with the same patch size;
 // returns the number of launches
 int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const double* d,
-                       double* Y, cudaStream_t s) {
+                       double* Y, int split, cudaStream_t s) {
   int launches = 0;
   for (int i = 0; i < n_groups;) {
     const DevPatchGroup& g = groups[i];
@@ -2102,12 +2106,12 @@ int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const 
     const DevPatchGroup* gp = groups + i;
     i += ng;
     if (g.n_patches == 0 && (ng == 1 || gp[1].n_patches == 0)) continue;
-    if (nc == 3 && g.np == 27) apply_dispatch<27, 28, 3>(gp, ng, d, Y, s);
-    else if (nc == 3 && g.np == 75) apply_dispatch<75, 76, 3>(gp, ng, d, Y, s);
-    else if (nc == 4 && g.np == 108) apply_dispatch<108, 108, 4>(gp, ng, d, Y, s);
-    else if (nc == 2 && g.np == 18) apply_dispatch<18, 18, 2>(gp, ng, d, Y, s);
-    else if (nc == 3 && g.np == 81) apply_dispatch<81, 82, 3>(gp, ng, d, Y, s);
-    else if (nc == 4 && g.np == 500) apply_dispatch<500, 500, 4>(gp, ng, d, Y, s);
+    if (nc == 3 && g.np == 27) apply_dispatch<27, 28, 3>(gp, ng, d, Y, split, s);
+    else if (nc == 3 && g.np == 75) apply_dispatch<75, 76, 3>(gp, ng, d, Y, split, s);
+    else if (nc == 4 && g.np == 108) apply_dispatch<108, 108, 4>(gp, ng, d, Y, split, s);
+    else if (nc == 2 && g.np == 18) apply_dispatch<18, 18, 2>(gp, ng, d, Y, split, s);
+    else if (nc == 3 && g.np == 81) apply_dispatch<81, 82, 3>(gp, ng, d, Y, split, s);
+    else if (nc == 4 && g.np == 500) apply_dispatch<500, 500, 4>(gp, ng, d, Y, split, s);
     else continue;
     ++launches;
   }

@@ -60,9 +60,11 @@ int64_t vanka_factorize_work(int np, int64_t n_patches);
 void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                             cudaStream_t s);
 // Y[p] = A_p^{-1} d[dofs_p] for every patch of the groups (consecutive groups
-// of one patch size share a launch); returns the number of launches
+// of one patch size share a launch); split: -1 default (column-split kernel
+// below 8,192 patches per launch), 0 never, 1 always; returns the number of
+// launches
 int launch_vanka_apply(const DevPatchGroup* groups, int n_groups, int nc, const double* d,
-                       double* Y, cudaStream_t s);
+                       double* Y, int split, cudaStream_t s);
 // x[dof] = (init_zero ? 0 : x[dof]) + omega * sum_{p ∋ dof} w[node] * Y[p, dof]
 void launch_vanka_gather(int64_t n_nodes, int nc, const int64_t* gptr, const int64_t* goff,
                          const double* weight, const double* Y, double* x, double omega,

@@ -162,6 +162,7 @@ struct Level {
   // sliced-ELL copy of the operator for the SpMV (nc == 3), see DevMatrix
   int64_t n_slices = 0, sell_slots = 0, sell_pslots = 0;
   int sell_lanes = 0;     // lanes per row (slice height 32 / lanes); 0: none
+  int apply_split = -1;   // Vanka apply form: -1 by patch count, 0 / 1 forced
   bool sell_dirty = false;
   DevBuf<int64_t> sell_off, sell_poff, sell_map, sell_pmap;
   DevBuf<int32_t> sell_col, sell_pcol;
@@ -403,7 +404,7 @@ struct MgHandle {
         dg[i].y_offset = g->y_offset;
       }
       int pr = prof_begin(1, l);
-      kernel_launches += launch_vanka_apply(dg.data(), ng, L.nc, d, L.Y.p, stream);
+      kernel_launches += launch_vanka_apply(dg.data(), ng, L.nc, d, L.Y.p, L.apply_split, stream);
       prof_end(pr);
     }
     int pr = prof_begin(2, l);
@@ -1487,6 +1488,17 @@ int alefsi_mg_set_sell(alefsi_mg h, int32_t level, int32_t lanes_per_row) {
   m->solve_valid = false;
   return ALEFSI_OK;
   ALEFSI_TRY_END
+}
+
+int alefsi_mg_set_apply_split(alefsi_mg h, int32_t level, int32_t split) {
+  MgHandle* m = H(h);
+  int rc = check_level(m, level);
+  if (rc) return rc;
+  if (split < -1 || split > 1) return fail(ALEFSI_ERR_ARG, "apply split: -1, 0 or 1");
+  m->lv[level].apply_split = split;
+  m->graph_valid = false;
+  m->solve_valid = false;
+  return ALEFSI_OK;
 }
 
 int alefsi_mg_spmv(alefsi_mg h, int32_t level, const double* x, const double* b, double* y) {

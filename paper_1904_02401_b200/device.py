@@ -242,6 +242,11 @@ class DeviceMgSolver:
         lanes per row (0: CSR half-warp kernel); see alefsi_mg_set_sell."""
         _lib.call("alefsi_mg_set_sell", self._h, level, int(lanes_per_row))
 
+    def set_apply_split(self, level, split):
+        """Vanka apply form of a level: -1 default, 0 unsplit, 1 column-split
+        (alefsi_mg_set_apply_split)."""
+        _lib.call("alefsi_mg_set_apply_split", self._h, level, int(split))
+
     def sweep(self, level, x, b):
         self._bind_torch_stream()
         _lib.call("alefsi_mg_vanka_sweep", self._h, level, x, b)
