@@ -28,6 +28,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 sys.path.insert(0, os.path.dirname(HERE))
 
 import golden_util  # noqa: E402
+
+HERE_OUT = [HERE]          # --out=DIR redirects the time-loop records
 import refbridge as rb  # noqa: E402
 from golden_util import sha, operator_checksums, vector_checksums  # noqa: E402
 from paper_1904_02401_b200 import workloads as W  # noqa: E402
@@ -172,16 +174,28 @@ def run_setup(name, with_operator=True):
     print(name, "setup digests written %.1fs" % out["ref_total_s"])
 
 
-def run_timestep(name, n_steps=None, tag=""):
+def run_timestep(name, n_steps=None, tag="", threads=0):
     """The reference's run_time_loop on a TimeStepping workload (config 4
-    family): per-step Newton/GMRES statistics and the final state."""
+    family): per-step Newton/GMRES statistics and the final state.
+    threads > 0: the reference's own patch-solve pool
+    (alefsi._parallel.set_threads) and the bitwise-neutral batch split of
+    numpy.einsum (baseline/ref_arm.threaded_einsum) — a different thread
+    configuration of the same computation (run-to-run envelope)."""
+    import contextlib
     ts = W.TIMESTEPPING[name]
     t0 = time.perf_counter()
-    U, records = rb.ref_timestepping(ts, n_steps)
+    ctx = contextlib.nullcontext()
+    if threads > 0:
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(HERE)), "baseline"))
+        import ref_arm
+        rb.ref()._parallel.set_threads(threads)
+        ctx = ref_arm.threaded_einsum(threads)
+    with ctx:
+        U, records = rb.ref_timestepping(ts, n_steps)
     out = {"workload": name, "source": "reference run_time_loop", "n_steps": len(records),
-           "records": records, "blas_threads": _blas_threads(),
+           "records": records, "blas_threads": _blas_threads(), "pool_threads": threads,
            "U_checksums": vector_checksums(U.reshape(-1)), "ref_wall_s": time.perf_counter() - t0}
-    with open(os.path.join(HERE, f"{name}{tag}.json"), "w") as f:
+    with open(os.path.join(HERE_OUT[0], f"{name}{tag}.json"), "w") as f:
         json.dump(out, f, indent=1)
     print(name, [r["newton_steps"] for r in records], "%.1fs" % out["ref_wall_s"])
 
@@ -192,11 +206,16 @@ if __name__ == "__main__":
     setup_only = "--setup-only" in args
     no_operator = "--no-operator" in args
     tag = next((a.split("=", 1)[1] for a in args if a.startswith("--tag=")), "")
+    steps = next((int(a.split("=", 1)[1]) for a in args if a.startswith("--steps=")), None)
+    threads = next((int(a.split("=", 1)[1]) for a in args if a.startswith("--threads=")), 0)
+    out_dir = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), None)
+    if out_dir:
+        HERE_OUT[0] = out_dir
     for a in args:
         if a.startswith("--"):
             continue
         if a in W.TIMESTEPPING:
-            run_timestep(a, tag=tag)
+            run_timestep(a, steps, tag=tag, threads=threads)
         elif setup_only:
             run_setup(a, with_operator=not no_operator)
         else:
