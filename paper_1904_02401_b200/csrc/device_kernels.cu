@@ -1595,23 +1595,51 @@ __global__ void gj_unscramble_kernel(double* M, int64_t n, const int64_t* perm,
   }
 }
 
-// warp per row; lane j sums columns j, j + 32, ... (fixed order).  A wider
-// 32-byte-load variant over padded rows (two accumulators per lane) was
-// measured: the changed summation order moved the 3d_tiny GMRES history
-// from ~1e-12 to 1.03e-10 of the reference's (its own BLAS-thread
-// run-to-run spread is 6e-11), for ~6 % of the config-0 solve.
+// warp per row; lane j sums columns j, j + 32, ... (fixed order: this
+// order is part of the parity — a two-accumulator variant moved the 3d_tiny
+// GMRES history from ~1e-12 to 1.03e-10 of the reference's, whose own
+// BLAS-thread spread there is 6e-11).  Rows padded to ld % 4 == 0 are read
+// as 32-byte quads, 128 columns per warp step, and handed to the lanes in
+// that order through a 1 KiB shared-memory transpose: the same FMA sequence
+// with a quarter of the load instructions.
 __global__ void __launch_bounds__(256) dense_matvec_kernel(int64_t n, const double* __restrict__ M,
+                                                           int64_t ld,
                                                            const double* __restrict__ x,
                                                            double* __restrict__ y) {
   pdl_entry();
-  const int lane = threadIdx.x & 31;
+  __shared__ double sq[8][128];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (row >= n) return;
-  const double* r = M + row * n;
+  const double* r = M + row * ld;
   double acc = 0.0;
-  for (int64_t j = lane; j < n; j += 32) acc = fma(__ldg(r + j), __ldg(x + j), acc);
+  for (int64_t c0 = 0; c0 < n; c0 += 128) {
+    const int64_t q = c0 + 4 * lane;
+    d4 v = {0.0, 0.0, 0.0, 0.0};
+    if (q < ld) v = ld256_ro(r + q);
+    sq[w][4 * lane] = v.x;
+    sq[w][4 * lane + 1] = v.y;
+    sq[w][4 * lane + 2] = v.z;
+    sq[w][4 * lane + 3] = v.w;
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int64_t j = c0 + lane + 32 * m;
+      if (j < n) acc = fma(sq[w][lane + 32 * m], __ldg(x + j), acc);
+    }
+    __syncwarp();
+  }
   acc = warp_sum(acc);
   if (lane == 0) y[row] = acc;
+}
+
+__global__ void pad_rows_kernel(int64_t n, const double* __restrict__ M, int64_t ld,
+                                double* __restrict__ P) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * ld;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ld, j = e - i * ld;
+    P[e] = j < n ? M[i * n + j] : 0.0;
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -2285,9 +2313,13 @@ int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStrea
   return 0;
 }
 
-void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
+void launch_dense_matvec(int64_t n, const double* M, int64_t ld, const double* x, double* y,
                          cudaStream_t s) {
-  launch_pdl(dense_matvec_kernel, grid_for(n * 32, 256), 256, 0, s, n, M, x, y);
+  launch_pdl(dense_matvec_kernel, grid_for(n * 32, 256), 256, 0, s, n, M, ld, x, y);
+}
+
+void launch_pad_rows(int64_t n, const double* M, int64_t ld, double* P, cudaStream_t s) {
+  pad_rows_kernel<<<(int)std::min<int64_t>(grid_for(n * ld, 256), 4096), 256, 0, s>>>(n, M, ld, P);
 }
 
 int launch_multi_dot(GmresCtl* ctl, int max_nvec, const double* V, int64_t ldv, const double* w,

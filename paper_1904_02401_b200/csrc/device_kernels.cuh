@@ -82,8 +82,11 @@ void launch_prolong_add(int64_t n_fine, int nc, const int64_t* ptr, const int32_
 // work: dense_inverse_work(n) doubles
 int dense_inverse(double* M, int64_t n, double* work, int64_t* status, cudaStream_t s);
 inline int64_t dense_inverse_work(int64_t n) { return 2 * n + 2 + 64 * n; }
-void launch_dense_matvec(int64_t n, const double* M, const double* x, double* y,
+// y = M x, M n x n stored with row stride ld (a multiple of 4)
+void launch_dense_matvec(int64_t n, const double* M, int64_t ld, const double* x, double* y,
                          cudaStream_t s);
+// P[i, j] = M[i, j] (row stride n -> ld), padding zero
+void launch_pad_rows(int64_t n, const double* M, int64_t ld, double* P, cudaStream_t s);
 
 // ---- GMRES (reference linsolve.py:41-115) with its state on the device, so
 // that a whole solve can run as one CUDA graph (conditional while node).

@@ -289,6 +289,10 @@ struct MgHandle {
   double omega = 0.8;
   std::vector<Level> lv;
   DevBuf<double> coarse_inv, coarse_work;
+  // the inverse with rows padded to a multiple of 4 doubles for the
+  // 32-byte loads of the coarse matvec
+  DevBuf<double> coarse_pad;
+  int64_t coarse_ld = 0;
   DevBuf<int64_t> status, coarse_status;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -418,7 +422,7 @@ struct MgHandle {
     Level& L = lv[l];
     if (l == 0) {
       int pr = prof_begin(5, l);
-      launch_dense_matvec(L.ndof(), coarse_inv.p, b, x, stream);
+      launch_dense_matvec(L.ndof(), coarse_pad.p, coarse_ld, b, x, stream);
       prof_end(pr);
       ++kernel_launches;
       return;
@@ -502,7 +506,7 @@ struct MgHandle {
   // buffers the captured V-cycle graph reads; a re-factorisation that keeps
   // them (same sizes: ensure() does not reallocate) keeps the graph valid
   std::vector<const void*> graph_buffers() const {
-    std::vector<const void*> v{coarse_inv.p};
+    std::vector<const void*> v{coarse_inv.p, coarse_pad.p};
     for (const auto& L : lv) {
       v.push_back(L.x.p);
       v.push_back(L.b.p);
@@ -541,6 +545,9 @@ struct MgHandle {
     if (dense_inverse(coarse_inv.p, n0, coarse_work.p, coarse_status.p, side_stream) != 0)
       return fail(ALEFSI_ERR_ARG, "coarse level too large for the dense inverse (" +
                                       std::to_string(n0) + " > 4096 dofs)");
+    coarse_ld = (n0 + 3) / 4 * 4;
+    CK(coarse_pad.ensure((size_t)n0 * coarse_ld));
+    launch_pad_rows(n0, coarse_inv.p, coarse_ld, coarse_pad.p, side_stream);
     CK(cudaGetLastError());
     CK(cudaEventRecord(side_out, side_stream));
     return ALEFSI_OK;
@@ -1560,7 +1567,7 @@ int alefsi_mg_coarse_solve(alefsi_mg h, const double* b, double* x) {
   MgHandle* m = H(h);
   if (!m) return fail(ALEFSI_ERR_ARG, "null handle");
   if (!m->factorized) return fail(ALEFSI_ERR_STATE, "coarse solve before factorize");
-  alefsi::launch_dense_matvec(m->lv[0].ndof(), m->coarse_inv.p, b, x, m->stream);
+  alefsi::launch_dense_matvec(m->lv[0].ndof(), m->coarse_pad.p, m->coarse_ld, b, x, m->stream);
   CKAPI(cudaGetLastError());
   return ALEFSI_OK;
   ALEFSI_TRY_END
