@@ -559,7 +559,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="3d_large")
-    ap.add_argument("--sweeps", type=int, default=20)
+    ap.add_argument("--sweeps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=900.0,
