@@ -507,24 +507,24 @@ def run_reference(args, rank, world):
     solves, hist = [], None
     budget = args.ref_budget_s
     warm = 0
-    # warm-up solves only while they are cheap relative to the budget
-    while warm < args.warmup:
-        ts = time.perf_counter()
-        x, st = ref_arm.solve(stack, b)
-        dt = time.perf_counter() - ts
-        warm += 1
-        hist = st
-        log(f"[reference] warm-up solve {dt:.1f}s, {st.iterations} iterations")
-        if dt * (args.warmup - warm + 1) > 0.25 * budget:
-            break
     tt = time.perf_counter()
+    # A CPU solve has no warm-up effect that matters once it takes minutes
+    # (no JIT, no lazy allocation in the timed code): a first solve longer
+    # than a tenth of the budget is the first timed solve, otherwise the
+    # requested warm-up solves run untimed first.
     while len(solves) < args.steps:
         ts = time.perf_counter()
         x, st = ref_arm.solve(stack, b)
-        solves.append(time.perf_counter() - ts)
+        dt = time.perf_counter() - ts
         hist = st
-        log(f"[reference] timed solve {solves[-1]:.1f}s, {st.iterations} iterations")
-        if time.perf_counter() - tt + solves[-1] > budget:
+        if not solves and warm < args.warmup and dt <= 0.1 * budget:
+            warm += 1
+            log(f"[reference] warm-up solve {dt:.1f}s, {st.iterations} iterations")
+            tt = time.perf_counter()
+            continue
+        solves.append(dt)
+        log(f"[reference] timed solve {dt:.1f}s, {st.iterations} iterations")
+        if time.perf_counter() - tt + dt > budget:
             break
     t_timed = time.perf_counter() - tt
     parity = check_against_golden(args.workload, hist.iterations, hist.residuals,

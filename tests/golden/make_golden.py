@@ -190,8 +190,15 @@ def run_timestep(name, n_steps=None, tag="", threads=0):
         import ref_arm
         rb.ref()._parallel.set_threads(threads)
         ctx = ref_arm.threaded_einsum(threads)
+    def progress(records):
+        # partial record after every time step (a multi-hour run survives an interruption)
+        with open(os.path.join(HERE_OUT[0], f"{name}{tag}.partial.json"), "w") as f:
+            json.dump({"workload": name, "records": records, "pool_threads": threads,
+                       "blas_threads": _blas_threads(),
+                       "ref_wall_s": time.perf_counter() - t0}, f, indent=1)
+
     with ctx:
-        U, records = rb.ref_timestepping(ts, n_steps)
+        U, records = rb.ref_timestepping(ts, n_steps, on_record=progress)
     out = {"workload": name, "source": "reference run_time_loop", "n_steps": len(records),
            "records": records, "blas_threads": _blas_threads(), "pool_threads": threads,
            "U_checksums": vector_checksums(U.reshape(-1)), "ref_wall_s": time.perf_counter() - t0}

@@ -48,7 +48,7 @@ def ref_problem(wl):
     return a.problem.FsiProblem(h, mats, flags)
 
 
-def ref_timestepping(ts, n_steps=None):
+def ref_timestepping(ts, n_steps=None, on_record=None):
     """The reference's own run_time_loop (newton.py:303-343) on a
     TimeStepping workload; returns (U, per-step records)."""
     a = ref()
@@ -76,6 +76,8 @@ def ref_timestepping(ts, n_steps=None):
                         "momentum_iters": [list(s.momentum_iters) for s in stats_list],
                         "extension_iters": [list(s.extension_iters) for s in stats_list],
                         "residuals": [[float(r) for r in s.residuals] for s in stats_list]})
+        if on_record is not None:
+            on_record(records)
     state, _ = a.newton.run_time_loop(prob, rtl, rnt, rlin, on_step=cb)
     return state.U, records
 
