@@ -863,6 +863,253 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
   }
 }
 
+
+// --------------------------------------------------------------------------
+// Gauss-Jordan inversion, second form ("panel-of-warp" layout): warp w owns
+// the CONTIGUOUS columns [w*CT, (w+1)*CT) of every row, the pivot loop is
+// unrolled over the CT column positions of the owning warp, so every column
+// access is a static register index (no select chains), the pivot row is
+// scaled and handed round inside each warp (shared-memory segment of the
+// warp, __syncwarp), and the owner of column k+1 updates that column first,
+// publishes it and chooses pivot k+1 (gj2_pick_pivot) while the other warps
+// eliminate: ONE block barrier per pivot step, the reciprocal computed once
+// per step.  The NP - 32*RTR tail rows are spread over the lanes of each
+// warp (TE elements per lane) and stay in registers.  Same pivot rule and the
+// same operations per element as vanka_factorize_cw_kernel.
+// --------------------------------------------------------------------------
+template <int NP, int RTR>
+__device__ __forceinline__ void gj2_pick_pivot(const double (&v)[RTR], double vt,
+                                               unsigned usedmask, int k1,
+                                               double* __restrict__ colk_n, int* piv_slot,
+                                               double* rp_slot, int* piv_of_step,
+                                               int* step_of_row, int64_t* status, int64_t pid1) {
+  constexpr int TAIL = NP - 32 * RTR;
+  const int ty = threadIdx.x & 31;
+  double best = -1.0;
+  int bi = NP;
+#pragma unroll
+  for (int i = 0; i < RTR; ++i) {
+    const double a = (usedmask >> i & 1u) ? -1.0 : fabs(v[i]);
+    if (a > best) { best = a; bi = ty + 32 * i; }
+  }
+  if (TAIL > 0 && ty < TAIL) {
+    const double a = (usedmask >> RTR & 1u) ? -1.0 : fabs(vt);
+    if (a > best) { best = a; bi = 32 * RTR + ty; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  const bool none = bi >= NP;          // no finite candidate (NaN column)
+  const double val = none ? 0.0 : colk_n[bi];
+  __syncwarp();
+  if (ty == 0 && !none) colk_n[bi] = 0.0;                    // f = 0 on the pivot row
+  if (ty == 0) {
+    if (none) {
+      bi = 0;
+      while (bi < NP - 1 && step_of_row[bi] >= 0) ++bi;
+    }
+    const double pv = none ? 0.0 : val;
+    if (pv == 0.0)
+      atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull, (unsigned long long)pid1);
+    *piv_slot = bi;
+    *rp_slot = pv != 0.0 ? 1.0 / pv : 0.0;       // singular: reported, result unused
+    piv_of_step[k1] = bi;
+    step_of_row[bi] = k1;
+  }
+}
+
+template <int NP, int NC, int W>
+__global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
+    DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
+    int ld, int64_t* status) {
+  constexpr int NPN = NP / NC, CT = NP / W, RTR = NP / 32, TAIL = NP - 32 * RTR, NT = 32 * W;
+  constexpr int CTP = (CT + 1) & ~1;                        // 16-byte aligned warp segments
+  // tail rows (one per lane < TAIL) in shared memory; the row stride keeps the
+  // 16-byte accesses of 8 consecutive lanes on distinct banks
+  constexpr int TS = W * CTP + 2;
+  static_assert(NP % W == 0 && RTR >= 1 && RTR <= 3 && TS % 2 == 0, "layout");
+  __shared__ __align__(16) double prow[W][CTP];
+  __shared__ __align__(16) double Mt[TAIL > 0 ? TAIL : 1][TS];
+  // column / pivot of step k in buffer (k % CT) % 3: a static index in the
+  // unrolled loop, never the buffer of the step before or after
+  static_assert((CT - 1) % 3 != 0, "buffer rotation");
+  __shared__ __align__(16) double colk[3][32 * RTR + 32];
+  __shared__ double rp_s[3];
+  __shared__ int piv_s[3];
+  __shared__ int piv_of_step[NP], step_of_row[NP];
+  __shared__ int32_t slotB[NPN * NPN], slotP[NPN * NPN];
+  const int tid = threadIdx.x, ty = tid & 31, w = tid >> 5;
+  const int64_t pid = blockIdx.x;
+  {
+    const int32_t* pn = nodes + pid * NPN;
+    for (int t = tid; t < NPN * NPN; t += NT) {
+      const int a = t / NPN, b = t - a * NPN;
+      const int64_t ra = pn[a];
+      const int32_t cb = pn[b];
+      int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
+      }
+      slotB[t] = (lo < A.indptr[ra + 1] && A.indices[lo] == cb) ? (int32_t)lo : -1;
+      int64_t sp = -1;
+      if (slotB[t] < 0 && A.pp_indptr != nullptr) {
+        lo = A.pp_indptr[ra];
+        hi = A.pp_indptr[ra + 1];
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
+        }
+        if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) sp = lo;
+      }
+      slotP[t] = (int32_t)sp;
+    }
+    for (int i = tid; i < NP; i += NT) step_of_row[i] = -1;
+    for (int i = tid; i < 3 * (32 * RTR + 32); i += NT) (&colk[0][0])[i] = 0.0;
+  }
+  __syncthreads();
+  auto entry = [&](int r, int c) -> double {
+    const int a = r / NC, ci = r - a * NC, b = c / NC, cj = c - b * NC;
+    const int t = a * NPN + b;
+    if (slotB[t] >= 0) return A.data[(int64_t)slotB[t] * (NC * NC) + ci * NC + cj];
+    if (ci == 0 && cj == 0 && slotP[t] >= 0) return A.pp_data[slotP[t]];
+    return 0.0;
+  };
+  const bool tl = TAIL > 0 && ty < TAIL;                    // this lane carries a tail row
+  double* const mt = &Mt[tl ? ty : 0][w * CTP];             // its segment of that row
+  double M[RTR][CT];
+#pragma unroll
+  for (int i = 0; i < RTR; ++i)
+#pragma unroll
+    for (int j = 0; j < CT; ++j) M[i][j] = entry(ty + 32 * i, w * CT + j);
+  if (tl) {
+#pragma unroll
+    for (int j = 0; j < CTP; ++j) mt[j] = j < CT ? entry(32 * RTR + ty, w * CT + j) : 0.0;
+  }
+  unsigned usedmask = 0;
+  if (w == 0) {
+    double c[RTR];
+#pragma unroll
+    for (int i = 0; i < RTR; ++i) {
+      c[i] = M[i][0];
+      colk[0][ty + 32 * i] = c[i];
+    }
+    double ct = 0.0;
+    if (tl) {
+      ct = mt[0];
+      colk[0][32 * RTR + ty] = ct;
+    }
+    __syncwarp();
+    gj2_pick_pivot<NP, RTR>(c, ct, usedmask, 0, colk[0], &piv_s[0], &rp_s[0], piv_of_step,
+                            step_of_row, status, pid + 1);
+  }
+  double* const myrow = prow[w];
+  for (int wo = 0; wo < W; ++wo) {
+    const bool own = (w == wo);
+#pragma unroll
+    for (int j = 0; j < CT; ++j) {
+      const int k = wo * CT + j;
+      const int jn = (j + 1 == CT) ? 0 : j + 1;            // static after unrolling
+      const int cb = j % 3, nb = jn % 3;
+      const int wn = (j + 1 == CT) ? wo + 1 : wo;
+      __syncthreads();
+      const int pr = piv_s[cb];
+      const double rp = rp_s[cb];
+      const int pl = pr & 31, pi = pr >> 5;
+      if (pl == ty) usedmask |= 1u << pi;
+      if (own) {
+        // column k restarts from 0: the elimination's fma then yields
+        // -f * (1/pivot) there (the pivot row entry becomes 1/pivot below)
+#pragma unroll
+        for (int i = 0; i < RTR; ++i) M[i][j] = 0.0;
+        if (tl) mt[j] = 0.0;
+      }
+      // the lane holding the pivot row scales it and hands this warp's
+      // segment to the warp's other lanes
+      if (ty == pl) {
+        if (pi < RTR) {
+#pragma unroll
+          for (int i = 0; i < RTR; ++i) {
+            if (pi == i) {
+#pragma unroll
+              for (int jj = 0; jj < CT; ++jj) {
+                double v = M[i][jj] * rp;
+                if (jj == j) v = own ? rp : v;
+                M[i][jj] = v;
+                myrow[jj] = v;
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < CT; ++jj) {
+            double v = mt[jj] * rp;
+            if (jj == j) v = own ? rp : v;
+            mt[jj] = v;
+            myrow[jj] = v;
+          }
+        }
+      }
+      __syncwarp();
+      double f[RTR];
+#pragma unroll
+      for (int i = 0; i < RTR; ++i) f[i] = -colk[cb][ty + 32 * i];
+      const double ft = -colk[cb][32 * RTR + (tl ? ty : 0)];
+      if (w == wn && k + 1 < NP) {
+        // next pivot column first: update it, publish it, choose its pivot
+        const double pvn = myrow[jn];
+        double c[RTR];
+#pragma unroll
+        for (int i = 0; i < RTR; ++i) {
+          c[i] = fma(f[i], pvn, M[i][jn]);
+          colk[nb][ty + 32 * i] = c[i];
+        }
+        double ct = 0.0;
+        if (tl) {
+          ct = fma(ft, pvn, mt[jn]);
+          colk[nb][32 * RTR + ty] = ct;
+        }
+        __syncwarp();
+        gj2_pick_pivot<NP, RTR>(c, ct, usedmask, k + 1, colk[nb], &piv_s[nb], &rp_s[nb],
+                                piv_of_step, step_of_row, status, pid + 1);
+      }
+#pragma unroll
+      for (int jj = 0; jj + 1 < CTP; jj += 2) {
+        const double2 pv = *reinterpret_cast<const double2*>(myrow + jj);
+#pragma unroll
+        for (int i = 0; i < RTR; ++i) {
+          M[i][jj] = fma(f[i], pv.x, M[i][jj]);
+          if (jj + 1 < CT) M[i][jj + 1] = fma(f[i], pv.y, M[i][jj + 1]);
+        }
+        if (tl) {
+          double2 t2 = *reinterpret_cast<double2*>(mt + jj);
+          t2.x = fma(ft, pv.x, t2.x);
+          t2.y = fma(ft, pv.y, t2.y);       // padding column: stays 0 (pv.y = 0)
+          *reinterpret_cast<double2*>(mt + jj) = t2;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* out = inv + pid * (int64_t)NP * ld;
+#pragma unroll
+  for (int i = 0; i < RTR; ++i)
+#pragma unroll
+    for (int j = 0; j < CT; ++j)
+      out[(int64_t)piv_of_step[w * CT + j] * ld + step_of_row[ty + 32 * i]] = M[i][j];
+  if (tl) {
+#pragma unroll
+    for (int j = 0; j < CT; ++j)
+      out[(int64_t)piv_of_step[w * CT + j] * ld + step_of_row[32 * RTR + ty]] = mt[j];
+  }
+  if (ld > NP)
+    for (int col = tid; col < NP; col += NT)
+      for (int r = NP; r < ld; ++r) out[(int64_t)col * ld + r] = 0.0;
+}
+
 // --------------------------------------------------------------------------
 // Large patches (2x2x2-cell macros in 3D: 500 x 500, the reference's default
 // solid blocking, newton.py:53-56): batched blocked Gauss-Jordan.  Each patch
@@ -2072,7 +2319,18 @@ void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* 
 
 constexpr int64_t kTailMinPatches = 8192;
 
+int g_fact_variant = 0;      // development A/B: 0 cw kernels, 9 / 12 pw kernel with W warps
+
+template <int NP, int NC, int W>
+void factorize_pw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
+                           cudaStream_t s) {
+  vanka_factorize_pw_kernel<NP, NC, W><<<(unsigned)g.n_patches, 32 * W, 0, s>>>(
+      A, g.n_patches, g.nodes, g.inv, g.ld, status);
+}
+
 }  // namespace
+
+extern "C" void alefsi_dev_set_fact_variant(int v) { g_fact_variant = v; }
 
 void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
                  cudaStream_t s) {
@@ -2109,6 +2367,10 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
     // CTA (178 registers, one CTA): config 1 80 -> 70 ms, bitwise equal
     factorize_cw_dispatch<75, 3, 8, 1>(A, g, status, s);
   }
+  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 9)
+    factorize_pw_dispatch<108, 4, 9>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 12)
+    factorize_pw_dispatch<108, 4, 12>(A, g, status, s);
   else if (A.nc == 4 && g.np == 108) {
     // two CTAs per SM; groups of >= 8192 patches (config 3: 134 -> 102 ms;
     // config 2, whose factorisation time is the coarse inverse's, unchanged)
