@@ -865,80 +865,71 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
 
 
 // --------------------------------------------------------------------------
-// Gauss-Jordan inversion, second form ("panel-of-warp" layout): warp w owns
-// the CONTIGUOUS columns [w*CT, (w+1)*CT) of every row, the pivot loop is
-// unrolled over the CT column positions of the owning warp, so every column
-// access is a static register index (no select chains), the pivot row is
-// scaled and handed round inside each warp (shared-memory segment of the
-// warp, __syncwarp), and the owner of column k+1 updates that column first,
-// publishes it and chooses pivot k+1 (gj2_pick_pivot) while the other warps
-// eliminate: ONE block barrier per pivot step, the reciprocal computed once
-// per step.  The NP - 32*RTR tail rows are spread over the lanes of each
-// warp (TE elements per lane) and stay in registers.  Same pivot rule and the
-// same operations per element as vanka_factorize_cw_kernel.
+// Gauss-Jordan inversion, second form: warp w owns the columns {w + W*j} of
+// every row (rows ty + 32*i in registers, the NP - 32*RTR tail rows in shared
+// memory, one per lane), ONE rolled loop over the pivot steps with one block
+// barrier per step:
+//  * the pivot row is scaled and handed round inside each warp (the lane
+//    holding it writes the warp's segment to shared memory, __syncwarp), so
+//    the only block-wide exchange is the pivot column;
+//  * the owner of column k+1 applies step k to that column first, publishes
+//    it and chooses pivot k+1 while the other warps eliminate; the choice is
+//    two warp-wide integer max reductions over a key (|value| with its low 7
+//    mantissa bits replaced by 127 - row: largest |value|, lowest row among
+//    values equal in the upper 45 mantissa bits — the getrf pivot up to
+//    last-bits ties);
+//  * after its elimination the owner resets the published column to the unit
+//    vector of the pivot row, so step k+1 needs no special case: the scaled
+//    pivot row carries 1/pivot there and the elimination writes -f/pivot.
 // --------------------------------------------------------------------------
-template <int NP, int RTR>
-__device__ __forceinline__ void gj2_pick_pivot(const double (&v)[RTR], double vt,
-                                               unsigned usedmask, int k1,
-                                               double* __restrict__ colk_n, int* piv_slot,
-                                               double* rp_slot, int* piv_of_step,
-                                               int* step_of_row, int64_t* status, int64_t pid1) {
-  constexpr int TAIL = NP - 32 * RTR;
-  const int ty = threadIdx.x & 31;
-  double best = -1.0;
-  int bi = NP;
-#pragma unroll
-  for (int i = 0; i < RTR; ++i) {
-    const double a = (usedmask >> i & 1u) ? -1.0 : fabs(v[i]);
-    if (a > best) { best = a; bi = ty + 32 * i; }
-  }
-  if (TAIL > 0 && ty < TAIL) {
-    const double a = (usedmask >> RTR & 1u) ? -1.0 : fabs(vt);
-    if (a > best) { best = a; bi = 32 * RTR + ty; }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-  }
-  const bool none = bi >= NP;          // no finite candidate (NaN column)
-  const double val = none ? 0.0 : colk_n[bi];
-  __syncwarp();
-  if (ty == 0 && !none) colk_n[bi] = 0.0;                    // f = 0 on the pivot row
-  if (ty == 0) {
-    if (none) {
-      bi = 0;
-      while (bi < NP - 1 && step_of_row[bi] >= 0) ++bi;
-    }
-    const double pv = none ? 0.0 : val;
-    if (pv == 0.0)
-      atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull, (unsigned long long)pid1);
-    *piv_slot = bi;
-    *rp_slot = pv != 0.0 ? 1.0 / pv : 0.0;       // singular: reported, result unused
-    piv_of_step[k1] = bi;
-    step_of_row[bi] = k1;
-  }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(a), "r"(parity) : "memory");
 }
 
-template <int NP, int NC, int W>
+struct alignas(16) GjPivot {
+  double rp;      // 1 / pivot (0 for a reported zero pivot)
+  int row, pad;
+};
+
+template <int NP, int NC, int W, bool ASYNC>
 __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
     DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, CT = NP / W, RTR = NP / 32, TAIL = NP - 32 * RTR, NT = 32 * W;
   constexpr int CTP = (CT + 1) & ~1;                        // 16-byte aligned warp segments
-  // tail rows (one per lane < TAIL) in shared memory; the row stride keeps the
-  // 16-byte accesses of 8 consecutive lanes on distinct banks
+  // tail rows: the row stride keeps the 16-byte accesses of 8 consecutive
+  // lanes on distinct banks
   constexpr int TS = W * CTP + 2;
-  static_assert(NP % W == 0 && RTR >= 1 && RTR <= 3 && TS % 2 == 0, "layout");
+  constexpr int CS = 32 * RTR + 32;
+  static_assert(NP % W == 0 && NP < 128 && RTR >= 1 && TS % 2 == 0, "layout");
   __shared__ __align__(16) double prow[W][CTP];
   __shared__ __align__(16) double Mt[TAIL > 0 ? TAIL : 1][TS];
-  // column / pivot of step k in buffer (k % CT) % 3: a static index in the
-  // unrolled loop, never the buffer of the step before or after
-  static_assert((CT - 1) % 3 != 0, "buffer rotation");
-  __shared__ __align__(16) double colk[3][32 * RTR + 32];
-  __shared__ double rp_s[3];
-  __shared__ int piv_s[3];
+  // ASYNC: no block barrier in the pivot loop.  The published column / pivot
+  // of step k sits in ring slot k % D; full[slot] is completed by the owner
+  // warp's 32 arrivals after publication, empty[slot] by one arrival per warp
+  // once its lanes have read the slot, so warps drift up to D - 1 steps apart
+  // and nobody waits for the owner's own elimination.
+  constexpr int D = ASYNC ? 4 : 2;
+  __shared__ __align__(16) double colk[D][CS];
+  __shared__ GjPivot pivot[D];
+  __shared__ uint64_t full_bar[D], empty_bar[D];
   __shared__ int piv_of_step[NP], step_of_row[NP];
   __shared__ int32_t slotB[NPN * NPN], slotP[NPN * NPN];
   const int tid = threadIdx.x, ty = tid & 31, w = tid >> 5;
@@ -967,8 +958,12 @@ __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
       }
       slotP[t] = (int32_t)sp;
     }
-    for (int i = tid; i < NP; i += NT) step_of_row[i] = -1;
-    for (int i = tid; i < 3 * (32 * RTR + 32); i += NT) (&colk[0][0])[i] = 0.0;
+    for (int i = tid; i < D * CS; i += NT) (&colk[0][0])[i] = 0.0;
+    for (int i = tid; i < W * CTP; i += NT) (&prow[0][0])[i] = 0.0;
+    if (ASYNC && tid < D) {
+      mbar_init(&full_bar[tid], 32);
+      mbar_init(&empty_bar[tid], W);
+    }
   }
   __syncthreads();
   auto entry = [&](int r, int c) -> double {
@@ -980,130 +975,184 @@ __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
   };
   const bool tl = TAIL > 0 && ty < TAIL;                    // this lane carries a tail row
   double* const mt = &Mt[tl ? ty : 0][w * CTP];             // its segment of that row
+  double* const myrow = prow[w];
   double M[RTR][CT];
 #pragma unroll
   for (int i = 0; i < RTR; ++i)
 #pragma unroll
-    for (int j = 0; j < CT; ++j) M[i][j] = entry(ty + 32 * i, w * CT + j);
+    for (int j = 0; j < CT; ++j) M[i][j] = entry(ty + 32 * i, j * W + w);
   if (tl) {
 #pragma unroll
-    for (int j = 0; j < CTP; ++j) mt[j] = j < CT ? entry(32 * RTR + ty, w * CT + j) : 0.0;
+    for (int j = 0; j < CTP; ++j) mt[j] = j < CT ? entry(32 * RTR + ty, j * W + w) : 0.0;
   }
   unsigned usedmask = 0;
+  // publication + pivot choice of column kk by its owner warp: c / ct are the
+  // column's current values in this lane's rows; returns the pivot row
+  auto pick = [&](int kk, const double (&c)[RTR], double ct) -> int {
+    const int slot = kk & (D - 1);
+    if (ASYNC && kk >= D) mbar_wait(&empty_bar[slot], ((kk / D) - 1) & 1);
+    double* cn = colk[slot];
+    unsigned long long key = 0ull;
+#pragma unroll
+    for (int i = 0; i < RTR; ++i) {
+      cn[ty + 32 * i] = c[i];
+      const unsigned long long kb =
+          ((unsigned long long)__double_as_longlong(fabs(c[i])) & ~127ull) |
+          (unsigned long long)(127 - (ty + 32 * i));
+      if (!(usedmask >> i & 1u) && kb > key) key = kb;
+    }
+    if (tl) {
+      cn[32 * RTR + ty] = ct;
+      const unsigned long long kb =
+          ((unsigned long long)__double_as_longlong(fabs(ct)) & ~127ull) |
+          (unsigned long long)(127 - (32 * RTR + ty));
+      if (!(usedmask >> RTR & 1u) && kb > key) key = kb;
+    }
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const int bi = min(127 - (int)(ml & 127u), NP - 1);
+    __syncwarp();
+    const double val = cn[bi];
+    // zero, NaN or infinite pivot: reported like the reference's singular block
+    const bool bad = val == 0.0 || mh >= 0x7ff00000u;
+    const double rp = bad ? 0.0 : 1.0 / val;
+    __syncwarp();
+    if (ty == 0) {
+      cn[bi] = 0.0;                              // f = 0 on the pivot row
+      GjPivot pn;
+      pn.rp = rp;
+      pn.row = bi;
+      pn.pad = 0;
+      pivot[slot] = pn;
+      piv_of_step[kk] = bi;
+      step_of_row[bi] = kk;
+      if (bad)
+        atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
+                  (unsigned long long)(pid + 1));
+    }
+    if (ASYNC) mbar_arrive(&full_bar[slot]);     // every lane after its own writes
+    return bi;
+  };
+#define ALEFSI_GJ_CASES(X)                                                                   \
+  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)           \
+  X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27)
+  static_assert(CT <= 28, "column switch");
+  // the published column becomes the unit vector of its pivot row
+  auto reset_column = [&](int jn, int bi) {
+    switch (jn) {
+#define ALEFSI_GJ_RESET(J)                                                                   \
+  case J:                                                                                    \
+    if constexpr (J < CT) {                                                                  \
+      _Pragma("unroll") for (int i = 0; i < RTR; ++i)                                        \
+          M[i][J] = (ty + 32 * i == bi) ? 1.0 : 0.0;                                         \
+    }                                                                                        \
+    break;
+      ALEFSI_GJ_CASES(ALEFSI_GJ_RESET)
+#undef ALEFSI_GJ_RESET
+      default: break;
+    }
+    if (tl) mt[jn] = (32 * RTR + ty == bi) ? 1.0 : 0.0;
+  };
   if (w == 0) {
     double c[RTR];
 #pragma unroll
-    for (int i = 0; i < RTR; ++i) {
-      c[i] = M[i][0];
-      colk[0][ty + 32 * i] = c[i];
-    }
-    double ct = 0.0;
-    if (tl) {
-      ct = mt[0];
-      colk[0][32 * RTR + ty] = ct;
-    }
-    __syncwarp();
-    gj2_pick_pivot<NP, RTR>(c, ct, usedmask, 0, colk[0], &piv_s[0], &rp_s[0], piv_of_step,
-                            step_of_row, status, pid + 1);
+    for (int i = 0; i < RTR; ++i) c[i] = M[i][0];
+    const int bi = pick(0, c, tl ? mt[0] : 0.0);
+    reset_column(0, bi);
   }
-  double* const myrow = prow[w];
-  for (int wo = 0; wo < W; ++wo) {
-    const bool own = (w == wo);
-#pragma unroll
-    for (int j = 0; j < CT; ++j) {
-      const int k = wo * CT + j;
-      const int jn = (j + 1 == CT) ? 0 : j + 1;            // static after unrolling
-      const int cb = j % 3, nb = jn % 3;
-      const int wn = (j + 1 == CT) ? wo + 1 : wo;
+  // iteration kk: elimination step k = kk - 1 and, by its owner, publication
+  // + pivot choice of column kk (kk < NP)
+#pragma unroll 1
+  for (int kk = 1; kk <= NP; ++kk) {
+    const int wn = kk % W, jn = kk / W;
+    const int cs = (kk - 1) & (D - 1);
+    if (ASYNC) {
+      __syncwarp();          // the warp is done with its pivot-row segment of the last step
+      mbar_wait(&full_bar[cs], ((kk - 1) / D) & 1);
+    } else {
       __syncthreads();
-      const int pr = piv_s[cb];
-      const double rp = rp_s[cb];
-      const int pl = pr & 31, pi = pr >> 5;
-      if (pl == ty) usedmask |= 1u << pi;
-      if (own) {
-        // column k restarts from 0: the elimination's fma then yields
-        // -f * (1/pivot) there (the pivot row entry becomes 1/pivot below)
-#pragma unroll
-        for (int i = 0; i < RTR; ++i) M[i][j] = 0.0;
-        if (tl) mt[j] = 0.0;
-      }
+    }
+    const GjPivot pv = pivot[cs];
+    const double* ck = colk[cs];
+    const int pl = pv.row & 31, pi = pv.row >> 5;
+    if (pl == ty) {
+      usedmask |= 1u << pi;
       // the lane holding the pivot row scales it and hands this warp's
       // segment to the warp's other lanes
-      if (ty == pl) {
-        if (pi < RTR) {
+      if (pi < RTR) {
 #pragma unroll
-          for (int i = 0; i < RTR; ++i) {
-            if (pi == i) {
+        for (int i = 0; i < RTR; ++i) {
+          if (pi == i) {
 #pragma unroll
-              for (int jj = 0; jj < CT; ++jj) {
-                double v = M[i][jj] * rp;
-                if (jj == j) v = own ? rp : v;
-                M[i][jj] = v;
-                myrow[jj] = v;
-              }
+            for (int jj = 0; jj < CT; ++jj) {
+              M[i][jj] *= pv.rp;
+              myrow[jj] = M[i][jj];
             }
           }
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < CT; ++jj) {
-            double v = mt[jj] * rp;
-            if (jj == j) v = own ? rp : v;
-            mt[jj] = v;
-            myrow[jj] = v;
-          }
         }
-      }
-      __syncwarp();
-      double f[RTR];
+      } else {
 #pragma unroll
-      for (int i = 0; i < RTR; ++i) f[i] = -colk[cb][ty + 32 * i];
-      const double ft = -colk[cb][32 * RTR + (tl ? ty : 0)];
-      if (w == wn && k + 1 < NP) {
-        // next pivot column first: update it, publish it, choose its pivot
-        const double pvn = myrow[jn];
-        double c[RTR];
-#pragma unroll
-        for (int i = 0; i < RTR; ++i) {
-          c[i] = fma(f[i], pvn, M[i][jn]);
-          colk[nb][ty + 32 * i] = c[i];
-        }
-        double ct = 0.0;
-        if (tl) {
-          ct = fma(ft, pvn, mt[jn]);
-          colk[nb][32 * RTR + ty] = ct;
-        }
-        __syncwarp();
-        gj2_pick_pivot<NP, RTR>(c, ct, usedmask, k + 1, colk[nb], &piv_s[nb], &rp_s[nb],
-                                piv_of_step, step_of_row, status, pid + 1);
-      }
-#pragma unroll
-      for (int jj = 0; jj + 1 < CTP; jj += 2) {
-        const double2 pv = *reinterpret_cast<const double2*>(myrow + jj);
-#pragma unroll
-        for (int i = 0; i < RTR; ++i) {
-          M[i][jj] = fma(f[i], pv.x, M[i][jj]);
-          if (jj + 1 < CT) M[i][jj + 1] = fma(f[i], pv.y, M[i][jj + 1]);
-        }
-        if (tl) {
-          double2 t2 = *reinterpret_cast<double2*>(mt + jj);
-          t2.x = fma(ft, pv.x, t2.x);
-          t2.y = fma(ft, pv.y, t2.y);       // padding column: stays 0 (pv.y = 0)
-          *reinterpret_cast<double2*>(mt + jj) = t2;
+        for (int jj = 0; jj < CT; ++jj) {
+          const double v = mt[jj] * pv.rp;
+          mt[jj] = v;
+          myrow[jj] = v;
         }
       }
     }
+    double f[RTR];
+#pragma unroll
+    for (int i = 0; i < RTR; ++i) f[i] = -ck[ty + 32 * i];
+    const double ft = -ck[32 * RTR + (tl ? ty : 0)];
+    __syncwarp();
+    if (ASYNC && ty == 0) mbar_arrive(&empty_bar[cs]);
+    int bi = -1;
+    if (w == wn && kk < NP) {
+      // next pivot column first: apply step k to it, publish it, choose its pivot
+      double c[RTR];
+      const double pvn = myrow[jn];
+      switch (jn) {
+#define ALEFSI_GJ_COL(J)                                                                     \
+  case J:                                                                                    \
+    if constexpr (J < CT) {                                                                  \
+      _Pragma("unroll") for (int i = 0; i < RTR; ++i) c[i] = fma(f[i], pvn, M[i][J]);        \
+    }                                                                                        \
+    break;
+        ALEFSI_GJ_CASES(ALEFSI_GJ_COL)
+#undef ALEFSI_GJ_COL
+        default: break;
+      }
+      bi = pick(kk, c, tl ? fma(ft, pvn, mt[jn]) : 0.0);
+    }
+#pragma unroll
+    for (int jj = 0; jj + 1 < CTP; jj += 2) {
+      const double2 p2 = *reinterpret_cast<const double2*>(myrow + jj);
+#pragma unroll
+      for (int i = 0; i < RTR; ++i) {
+        M[i][jj] = fma(f[i], p2.x, M[i][jj]);
+        if (jj + 1 < CT) M[i][jj + 1] = fma(f[i], p2.y, M[i][jj + 1]);
+      }
+      if (tl) {
+        double2 t2 = *reinterpret_cast<double2*>(mt + jj);
+        t2.x = fma(ft, p2.x, t2.x);
+        t2.y = fma(ft, p2.y, t2.y);       // padding column: stays 0 (p2.y = 0)
+        *reinterpret_cast<double2*>(mt + jj) = t2;
+      }
+    }
+    if (bi >= 0) reset_column(jn, bi);
   }
+#undef ALEFSI_GJ_CASES
   __syncthreads();
   double* out = inv + pid * (int64_t)NP * ld;
 #pragma unroll
   for (int i = 0; i < RTR; ++i)
 #pragma unroll
     for (int j = 0; j < CT; ++j)
-      out[(int64_t)piv_of_step[w * CT + j] * ld + step_of_row[ty + 32 * i]] = M[i][j];
+      out[(int64_t)piv_of_step[j * W + w] * ld + step_of_row[ty + 32 * i]] = M[i][j];
   if (tl) {
 #pragma unroll
     for (int j = 0; j < CT; ++j)
-      out[(int64_t)piv_of_step[w * CT + j] * ld + step_of_row[32 * RTR + ty]] = mt[j];
+      out[(int64_t)piv_of_step[j * W + w] * ld + step_of_row[32 * RTR + ty]] = mt[j];
   }
   if (ld > NP)
     for (int col = tid; col < NP; col += NT)
@@ -2321,10 +2370,10 @@ constexpr int64_t kTailMinPatches = 8192;
 
 int g_fact_variant = 0;      // development A/B: 0 cw kernels, 9 / 12 pw kernel with W warps
 
-template <int NP, int NC, int W>
+template <int NP, int NC, int W, bool ASYNC = false>
 void factorize_pw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                            cudaStream_t s) {
-  vanka_factorize_pw_kernel<NP, NC, W><<<(unsigned)g.n_patches, 32 * W, 0, s>>>(
+  vanka_factorize_pw_kernel<NP, NC, W, ASYNC><<<(unsigned)g.n_patches, 32 * W, 0, s>>>(
       A, g.n_patches, g.nodes, g.inv, g.ld, status);
 }
 
@@ -2371,6 +2420,16 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
     factorize_pw_dispatch<108, 4, 9>(A, g, status, s);
   else if (A.nc == 4 && g.np == 108 && g_fact_variant == 12)
     factorize_pw_dispatch<108, 4, 12>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 6)
+    factorize_pw_dispatch<108, 4, 6>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 4)
+    factorize_pw_dispatch<108, 4, 4>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 106)
+    factorize_pw_dispatch<108, 4, 6, true>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 104)
+    factorize_pw_dispatch<108, 4, 4, true>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 109)
+    factorize_pw_dispatch<108, 4, 9, true>(A, g, status, s);
   else if (A.nc == 4 && g.np == 108) {
     // two CTAs per SM; groups of >= 8192 patches (config 3: 134 -> 102 ms;
     // config 2, whose factorisation time is the coarse inverse's, unchanged)

@@ -24,7 +24,7 @@ from paper_1904_02401_b200 import _lib, workloads as W  # noqa: E402
 
 def main():
     names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["3d_small"]
-    variants = [0, 12, 9]
+    variants = [int(a[11:]) for a in sys.argv if a.startswith("--variants=")] or [0, 6, 106, 104]
     lib = _lib.load()
     setv = lib.alefsi_dev_set_fact_variant
     setv.argtypes = [ctypes.c_int]
