@@ -649,20 +649,15 @@ struct IntC {
 // next pivot with a warp-local argmax right after its own share of the
 // step-k elimination, overlapped with the other warps' eliminations: two
 // block barriers per pivot step, no single-warp phase on the critical path.
-// TAIL > 0 (NPAT = 1): the last register row holds only TAIL real rows
-// (108 = 3 x 32 + 12); those rows live in shared memory instead, which
-// brings the kernel under the register budget of two CTAs per SM, so two
-// patches' pivot chains overlap.  Same operations: bitwise-equal inverses.
-template <int NP, int NC, int W, int NPAT, int TAIL = 0>
-__global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_kernel(
+// Used for the small patch sizes (18, 27, 81); 75 and 108 use the second form
+// below.
+template <int NP, int NC, int W, int NPAT>
+__global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
     DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, RT = (NP + 31) / 32, CT = (NP + W - 1) / W, NT = 32 * W;
   static_assert(RT <= 4, "pivot-row scaling covers up to 4 register rows");
   constexpr int NR = 32 * RT, NCOL = W * CT;               // padded row / column counts
-  constexpr int RTR = TAIL > 0 ? RT - 1 : RT;               // register rows
-  static_assert(TAIL == 0 || (NPAT == 1 && TAIL == NP - 32 * RTR), "tail rows");
-  __shared__ double Mt[TAIL > 0 ? TAIL : 1][NCOL + 1];     // +1: conflict-free rows
   __shared__ int32_t slotB[NPAT][NPN * NPN], slotP[NPAT][NPN * NPN];
   __shared__ double colk[NPAT][2][NR], prow[NPAT][NCOL], pivval[NPAT];
   __shared__ int used[NPAT][NP], piv_of_step[NPAT][NP], step_of_row[NPAT][NP];
@@ -705,7 +700,7 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
   }
   for (int i = tid; i < NPAT * NP; i += NT) used[i / NP][i % NP] = 0;
   __syncthreads();
-  double M[NPAT][RTR][CT];
+  double M[NPAT][RT][CT];
 #pragma unroll
   for (int q = 0; q < NPAT; ++q)
 #pragma unroll
@@ -721,9 +716,7 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
           if (slotB[q][t] >= 0) v = A.data[(int64_t)slotB[q][t] * (NC * NC) + ci * NC + cj];
           else if (ci == 0 && cj == 0 && slotP[q][t] >= 0) v = A.pp_data[slotP[q][t]];
         }
-        if constexpr (TAIL == 0) M[q][i][j] = v;
-        else if (i < RTR) M[q][i < RTR ? i : 0][j] = v;
-        else if (ty < TAIL) Mt[ty][c] = v;
+        M[q][i][j] = v;
       }
   // owner warp of column k: publish it and choose its pivot (largest |.| of
   // the unused rows, lowest index on ties)
@@ -738,18 +731,12 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
       for (int i = 0; i < RT; ++i) {
         const int r = ty + 32 * i;
         double v = 0.0;
-        if (TAIL == 0 || i < RTR) {
 #pragma unroll
-          for (int j = 0; j < CT; ++j) {
-            const int ir = TAIL == 0 ? i : (i < RTR ? i : 0);
-            if (j == jk) v = M[q][ir][j];
-            // column k restarts from 0: the elimination's fma then yields
-            // -f * (1/pivot) there, with no per-element select
-            M[q][ir][j] = (j == jk) ? 0.0 : M[q][ir][j];
-          }
-        } else if (ty < TAIL) {
-          v = Mt[ty][k];
-          Mt[ty][k] = 0.0;
+        for (int j = 0; j < CT; ++j) {
+          if (j == jk) v = M[q][i][j];
+          // column k restarts from 0: the elimination's fma then yields
+          // -f * (1/pivot) there, with no per-element select
+          M[q][i][j] = (j == jk) ? 0.0 : M[q][i][j];
         }
         if (r < NP) {
           colk[q][k & 1][r] = v;
@@ -796,15 +783,9 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
 #pragma unroll
           for (int j = 0; j < CT; ++j) {
             const int c = w + W * j;
-            if constexpr (i < RTR) {
-              const double v = (c == k) ? rp[q] : M[q][i][j] * rp[q];
-              M[q][i][j] = v;
-              if (c < NP) prow[q][c] = v;
-            } else {
-              const double v = (c == k) ? rp[q] : Mt[ty][c] * rp[q];
-              Mt[ty][c] = v;
-              if (c < NP) prow[q][c] = v;
-            }
+            const double v = (c == k) ? rp[q] : M[q][i][j] * rp[q];
+            M[q][i][j] = v;
+            if (c < NP) prow[q][c] = v;
           }
         };
         switch (pr[q] >> 5) {
@@ -828,17 +809,10 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
 #pragma unroll
       for (int j = 0; j < CT; ++j) pv[j] = prow[q][w + W * j];
 #pragma unroll
-      for (int i = 0; i < RTR; ++i) {
+      for (int i = 0; i < RT; ++i) {
         const double nf = -ck[ty + 32 * i];
 #pragma unroll
         for (int j = 0; j < CT; ++j) M[q][i][j] = fma(nf, pv[j], M[q][i][j]);
-      }
-      if constexpr (TAIL > 0) {
-        if (ty < TAIL) {
-          const double nf = -ck[ty + 32 * RTR];
-#pragma unroll
-          for (int j = 0; j < CT; ++j) Mt[ty][w + W * j] = fma(nf, pv[j], Mt[ty][w + W * j]);
-        }
       }
     }
     if (k + 1 < NP) owner_step(k + 1);
@@ -854,8 +828,7 @@ __global__ void __launch_bounds__(32 * W, TAIL > 0 ? 2 : 0) vanka_factorize_cw_k
       for (int j = 0; j < CT; ++j) {
         const int r = ty + 32 * i, c = w + W * j;
         if (r < NP && c < NP)
-          out[(int64_t)piv_of_step[q][c] * ld + step_of_row[q][r]] =
-              (TAIL == 0 || i < RTR) ? M[q][TAIL == 0 ? i : (i < RTR ? i : 0)][j] : Mt[ty][c];
+          out[(int64_t)piv_of_step[q][c] * ld + step_of_row[q][r]] = M[q][i][j];
       }
     if (ld > NP)
       for (int col = tid; col < NP; col += NT)
@@ -908,29 +881,30 @@ struct alignas(16) GjPivot {
   int row, pad;
 };
 
-template <int NP, int NC, int W, bool ASYNC>
-__global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
+template <int NP, int NC, int W, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB) vanka_factorize_pw_kernel(
     DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, CT = NP / W, RTR = NP / 32, TAIL = NP - 32 * RTR, NT = 32 * W;
   constexpr int CTP = (CT + 1) & ~1;                        // 16-byte aligned warp segments
   // tail rows: the row stride keeps the 16-byte accesses of 8 consecutive
   // lanes on distinct banks
-  constexpr int TS = W * CTP + 2;
+  constexpr int TS = (W * CTP + 1) / 4 * 4 + 2;
   constexpr int CS = 32 * RTR + 32;
   static_assert(NP % W == 0 && NP < 128 && RTR >= 1 && TS % 2 == 0, "layout");
   __shared__ __align__(16) double prow[W][CTP];
   __shared__ __align__(16) double Mt[TAIL > 0 ? TAIL : 1][TS];
-  // ASYNC: no block barrier in the pivot loop.  The published column / pivot
-  // of step k sits in ring slot k % D; full[slot] is completed by the owner
-  // warp's 32 arrivals after publication, empty[slot] by one arrival per warp
-  // once its lanes have read the slot, so warps drift up to D - 1 steps apart
-  // and nobody waits for the owner's own elimination.
-  constexpr int D = ASYNC ? 4 : 2;
+  // No block barrier in the pivot loop.  The published column / pivot of step
+  // k sits in ring slot k % D; full[slot] is completed by the owner warp's 32
+  // arrivals after publication, empty[slot] by one arrival per warp once its
+  // lanes have read the slot: nobody waits for the owner's own elimination
+  // (deeper rings measured equal: the chain of pivot choices sets the pace).
+  constexpr int D = 2;
   __shared__ __align__(16) double colk[D][CS];
   __shared__ GjPivot pivot[D];
   __shared__ uint64_t full_bar[D], empty_bar[D];
   __shared__ int piv_of_step[NP], step_of_row[NP];
+  __shared__ double rp_of_row[NP];                         // pending row factors
   __shared__ int32_t slotB[NPN * NPN], slotP[NPN * NPN];
   const int tid = threadIdx.x, ty = tid & 31, w = tid >> 5;
   const int64_t pid = blockIdx.x;
@@ -960,7 +934,7 @@ __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
     }
     for (int i = tid; i < D * CS; i += NT) (&colk[0][0])[i] = 0.0;
     for (int i = tid; i < W * CTP; i += NT) (&prow[0][0])[i] = 0.0;
-    if (ASYNC && tid < D) {
+    if (tid < D) {
       mbar_init(&full_bar[tid], 32);
       mbar_init(&empty_bar[tid], W);
     }
@@ -990,7 +964,7 @@ __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
   // column's current values in this lane's rows; returns the pivot row
   auto pick = [&](int kk, const double (&c)[RTR], double ct) -> int {
     const int slot = kk & (D - 1);
-    if (ASYNC && kk >= D) mbar_wait(&empty_bar[slot], ((kk / D) - 1) & 1);
+    if (kk >= D) mbar_wait(&empty_bar[slot], ((kk / D) - 1) & 1);
     double* cn = colk[slot];
     unsigned long long key = 0ull;
 #pragma unroll
@@ -1027,11 +1001,12 @@ __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
       pivot[slot] = pn;
       piv_of_step[kk] = bi;
       step_of_row[bi] = kk;
+      rp_of_row[bi] = rp;
       if (bad)
         atomicCAS(reinterpret_cast<unsigned long long*>(status), 0ull,
                   (unsigned long long)(pid + 1));
     }
-    if (ASYNC) mbar_arrive(&full_bar[slot]);     // every lane after its own writes
+    mbar_arrive(&full_bar[slot]);                // every lane after its own writes
     return bi;
   };
 #define ALEFSI_GJ_CASES(X)                                                                   \
@@ -1067,45 +1042,38 @@ __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
   for (int kk = 1; kk <= NP; ++kk) {
     const int wn = kk % W, jn = kk / W;
     const int cs = (kk - 1) & (D - 1);
-    if (ASYNC) {
-      __syncwarp();          // the warp is done with its pivot-row segment of the last step
-      mbar_wait(&full_bar[cs], ((kk - 1) / D) & 1);
-    } else {
-      __syncthreads();
-    }
+    __syncwarp();            // the warp is done with its pivot-row segment of the last step
+    mbar_wait(&full_bar[cs], ((kk - 1) / D) & 1);
     const GjPivot pv = pivot[cs];
     const double* ck = colk[cs];
     const int pl = pv.row & 31, pi = pv.row >> 5;
     if (pl == ty) {
       usedmask |= 1u << pi;
-      // the lane holding the pivot row scales it and hands this warp's
-      // segment to the warp's other lanes
+      // the lane holding the pivot row hands this warp's segment of it to the
+      // warp's other lanes, unscaled: 1/pivot goes into the multipliers, and
+      // the row keeps its own factor 1/pivot pending until the write-out (a
+      // row with a pending factor updates itself consistently: its published
+      // column entries are unscaled too)
       if (pi < RTR) {
 #pragma unroll
         for (int i = 0; i < RTR; ++i) {
           if (pi == i) {
 #pragma unroll
-            for (int jj = 0; jj < CT; ++jj) {
-              M[i][jj] *= pv.rp;
-              myrow[jj] = M[i][jj];
-            }
+            for (int jj = 0; jj < CT; ++jj) myrow[jj] = M[i][jj];
           }
         }
       } else {
 #pragma unroll
-        for (int jj = 0; jj < CT; ++jj) {
-          const double v = mt[jj] * pv.rp;
-          mt[jj] = v;
-          myrow[jj] = v;
-        }
+        for (int jj = 0; jj + 1 < CTP; jj += 2)
+          *reinterpret_cast<double2*>(myrow + jj) = *reinterpret_cast<const double2*>(mt + jj);
       }
     }
     double f[RTR];
 #pragma unroll
-    for (int i = 0; i < RTR; ++i) f[i] = -ck[ty + 32 * i];
-    const double ft = -ck[32 * RTR + (tl ? ty : 0)];
+    for (int i = 0; i < RTR; ++i) f[i] = -ck[ty + 32 * i] * pv.rp;
+    const double ft = -ck[32 * RTR + (tl ? ty : 0)] * pv.rp;
     __syncwarp();
-    if (ASYNC && ty == 0) mbar_arrive(&empty_bar[cs]);
+    if (ty == 0) mbar_arrive(&empty_bar[cs]);
     int bi = -1;
     if (w == wn && kk < NP) {
       // next pivot column first: apply step k to it, publish it, choose its pivot
@@ -1148,11 +1116,13 @@ __global__ void __launch_bounds__(32 * W, 2) vanka_factorize_pw_kernel(
   for (int i = 0; i < RTR; ++i)
 #pragma unroll
     for (int j = 0; j < CT; ++j)
-      out[(int64_t)piv_of_step[j * W + w] * ld + step_of_row[ty + 32 * i]] = M[i][j];
+      out[(int64_t)piv_of_step[j * W + w] * ld + step_of_row[ty + 32 * i]] =
+          M[i][j] * rp_of_row[ty + 32 * i];
   if (tl) {
 #pragma unroll
     for (int j = 0; j < CT; ++j)
-      out[(int64_t)piv_of_step[j * W + w] * ld + step_of_row[32 * RTR + ty]] = mt[j];
+      out[(int64_t)piv_of_step[j * W + w] * ld + step_of_row[32 * RTR + ty]] =
+          mt[j] * rp_of_row[32 * RTR + ty];
   }
   if (ld > NP)
     for (int col = tid; col < NP; col += NT)
@@ -2358,28 +2328,22 @@ void factorize_big(const DevMatrix& A, const DevPatchGroup& g, int64_t* status, 
   big_finish_kernel<<<dim3(32, (unsigned)P), 256, 0, s>>>(n, M, pstatus, status);
 }
 
-template <int NP, int NC, int W, int NPAT, int TAIL = 0>
+template <int NP, int NC, int W, int NPAT>
 void factorize_cw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                            cudaStream_t s) {
   const unsigned grid = (unsigned)((g.n_patches + NPAT - 1) / NPAT);
-  vanka_factorize_cw_kernel<NP, NC, W, NPAT, TAIL><<<grid, 32 * W, 0, s>>>(
+  vanka_factorize_cw_kernel<NP, NC, W, NPAT><<<grid, 32 * W, 0, s>>>(
       A, g.n_patches, g.nodes, g.inv, g.ld, status);
 }
 
-constexpr int64_t kTailMinPatches = 8192;
-
-int g_fact_variant = 0;      // development A/B: 0 cw kernels, 9 / 12 pw kernel with W warps
-
-template <int NP, int NC, int W, bool ASYNC = false>
+template <int NP, int NC, int W, int MINB>
 void factorize_pw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                            cudaStream_t s) {
-  vanka_factorize_pw_kernel<NP, NC, W, ASYNC><<<(unsigned)g.n_patches, 32 * W, 0, s>>>(
+  vanka_factorize_pw_kernel<NP, NC, W, MINB><<<(unsigned)g.n_patches, 32 * W, 0, s>>>(
       A, g.n_patches, g.nodes, g.inv, g.ld, status);
 }
 
 }  // namespace
-
-extern "C" void alefsi_dev_set_fact_variant(int v) { g_fact_variant = v; }
 
 void launch_spmv(const DevMatrix& A, const double* x, const double* b, double* y, int mode,
                  cudaStream_t s) {
@@ -2411,32 +2375,11 @@ void launch_vanka_factorize(const DevMatrix& A, const DevPatchGroup& g, int64_t*
                             cudaStream_t s) {
   if (g.n_patches == 0) return;
   if (A.nc == 3 && g.np == 27) factorize_cw_dispatch<27, 3, 3, 2>(A, g, status, s);
-  else if (A.nc == 3 && g.np == 75) {
-    // one patch per CTA (118 registers, two CTAs per SM) instead of two per
-    // CTA (178 registers, one CTA): config 1 80 -> 70 ms, bitwise equal
-    factorize_cw_dispatch<75, 3, 8, 1>(A, g, status, s);
-  }
-  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 9)
-    factorize_pw_dispatch<108, 4, 9>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 12)
-    factorize_pw_dispatch<108, 4, 12>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 6)
-    factorize_pw_dispatch<108, 4, 6>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 4)
-    factorize_pw_dispatch<108, 4, 4>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 106)
-    factorize_pw_dispatch<108, 4, 6, true>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 104)
-    factorize_pw_dispatch<108, 4, 4, true>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108 && g_fact_variant == 109)
-    factorize_pw_dispatch<108, 4, 9, true>(A, g, status, s);
-  else if (A.nc == 4 && g.np == 108) {
-    // two CTAs per SM; groups of >= 8192 patches (config 3: 134 -> 102 ms;
-    // config 2, whose factorisation time is the coarse inverse's, unchanged)
-    if (g.n_patches >= kTailMinPatches)
-      factorize_cw_dispatch<108, 4, 12, 1, 12>(A, g, status, s);
-    else factorize_cw_dispatch<108, 4, 12, 1>(A, g, status, s);
-  }
+  // 75x75 and 108x108: the second form (fat warps, mbarrier ring).  Config 3
+  // Vanka + coarse factorisation 103.3 -> 61.2 ms, config 1 50.3 -> 43.1 ms
+  // against the column-strided kernel with two block barriers per step.
+  else if (A.nc == 3 && g.np == 75) factorize_pw_dispatch<75, 3, 5, 3>(A, g, status, s);
+  else if (A.nc == 4 && g.np == 108) factorize_pw_dispatch<108, 4, 6, 2>(A, g, status, s);
   else if (A.nc == 2 && g.np == 18) factorize_cw_dispatch<18, 2, 2, 2>(A, g, status, s);
   else if (A.nc == 3 && g.np == 81) factorize_cw_dispatch<81, 3, 9, 2>(A, g, status, s);
   else if (A.nc == 4 && g.np == 500 && g.ld == g.np && g.work != nullptr)
