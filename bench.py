@@ -112,6 +112,9 @@ def peaks():
 
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML from
+    a background thread every 10 ms (so that a 0.1 s timed region of the small
+    workloads still yields ~10 samples), else `nvidia-smi -lms 200`."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -119,8 +122,58 @@ class ClockSampler:
     def __init__(self, index=0):
         self.index = index
         self.proc = None
+        self.thread = None
+        self.lines = []
+
+    def _nvml_loop(self, nv, handle, stop):
+        names = [("hw_slowdown", nv.nvmlClocksEventReasonHwSlowdown),
+                 ("hw_thermal_slowdown", nv.nvmlClocksEventReasonHwThermalSlowdown),
+                 ("sw_thermal_slowdown", nv.nvmlClocksEventReasonSwThermalSlowdown),
+                 ("sw_power_cap", nv.nvmlClocksEventReasonSwPowerCap)]
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(handle, nv.NVML_CLOCK_SM)
+        except Exception:
+            mx = 0
+        while not stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(handle)
+                self.lines.append(",".join([str(sm), str(mx)] + [
+                    "Active" if mask & bit else "Not Active" for _, bit in names]))
+            except Exception:
+                break
+            stop.wait(0.01)
 
     def __enter__(self):
+        try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            # NVML enumerates all boards: map the CUDA device through its PCI bus id
+            import torch
+            bus = torch.cuda.get_device_properties(self.index).pci_bus_id \
+                if hasattr(torch.cuda.get_device_properties(self.index), "pci_bus_id") else None
+            handle = None
+            if bus is not None:
+                for i in range(nv.nvmlDeviceGetCount()):
+                    h = nv.nvmlDeviceGetHandleByIndex(i)
+                    if nv.nvmlDeviceGetPciInfo(h).bus == bus:
+                        handle = h
+                        break
+            if handle is None:
+                visible = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                ids = [v for v in visible.split(",") if v.strip().isdigit()]
+                phys = int(ids[self.index]) if self.index < len(ids) else self.index
+                handle = nv.nvmlDeviceGetHandleByIndex(phys)
+            nv.nvmlDeviceGetClockInfo(handle, nv.NVML_CLOCK_SM)
+            nv.nvmlDeviceGetCurrentClocksEventReasons(handle)
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._nvml_loop,
+                                           args=(nv, handle, self.stop), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -131,6 +184,10 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            return
         self.lines = []
         if self.proc is not None:
             self.proc.terminate()
@@ -154,10 +211,12 @@ class ClockSampler:
             for n, v in zip(names, parts[2:]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
+        src = "nvml, 10 ms" if self.thread is not None else "nvidia-smi -lms 200"
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "sampler": src}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "sampler": src}
 
 
 def max_over_ranks(values, world, device=None):
