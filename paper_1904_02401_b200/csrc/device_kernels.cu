@@ -837,6 +837,41 @@ __global__ void __launch_bounds__(32 * W) vanka_factorize_cw_kernel(
 }
 
 
+// Operator slots of every (row node, column node) pair of every patch, found
+// once per sparsity pattern: >= 0 block slot, <= -2 pressure-extension entry
+// -(v + 2), -1 structurally zero (the reference's pattern.slots_for,
+// linsolve.py:124-126).  The factorisation kernels read their patch's table
+// with one coalesced load instead of npn^2 binary searches per factorisation.
+__global__ void patch_slots_kernel(DevMatrix A, int64_t n_patches, int npn,
+                                   const int32_t* __restrict__ nodes,
+                                   int32_t* __restrict__ slots) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)npn * npn;
+  if (t >= n_patches * per) return;
+  const int64_t p = t / per;
+  const int r = (int)(t - p * per), a = r / npn, b = r - a * npn;
+  const int64_t ra = nodes[p * npn + a];
+  const int32_t cb = nodes[p * npn + b];
+  int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
+  }
+  int32_t v = -1;
+  if (lo < A.indptr[ra + 1] && A.indices[lo] == cb) {
+    v = (int32_t)lo;
+  } else if (A.pp_indptr != nullptr) {
+    lo = A.pp_indptr[ra];
+    hi = A.pp_indptr[ra + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
+    }
+    if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) v = -(int32_t)lo - 2;
+  }
+  slots[t] = v;
+}
+
 // --------------------------------------------------------------------------
 // Gauss-Jordan inversion, second form: warp w owns the columns {w + W*j} of
 // every row (rows ty + 32*i in registers, the NP - 32*RTR tail rows in shared
@@ -883,7 +918,7 @@ struct alignas(16) GjPivot {
 
 template <int NP, int NC, int W, int MINB>
 __global__ void __launch_bounds__(32 * W, MINB) vanka_factorize_pw_kernel(
-    DevMatrix A, int64_t n_patches, const int32_t* __restrict__ nodes, double* __restrict__ inv,
+    DevMatrix A, int64_t n_patches, const int32_t* __restrict__ slots, double* __restrict__ inv,
     int ld, int64_t* status) {
   constexpr int NPN = NP / NC, CT = NP / W, RTR = NP / 32, TAIL = NP - 32 * RTR, NT = 32 * W;
   constexpr int CTP = (CT + 1) & ~1;                        // 16-byte aligned warp segments
@@ -909,28 +944,11 @@ __global__ void __launch_bounds__(32 * W, MINB) vanka_factorize_pw_kernel(
   const int tid = threadIdx.x, ty = tid & 31, w = tid >> 5;
   const int64_t pid = blockIdx.x;
   {
-    const int32_t* pn = nodes + pid * NPN;
+    const int32_t* ps = slots + pid * (NPN * NPN);
     for (int t = tid; t < NPN * NPN; t += NT) {
-      const int a = t / NPN, b = t - a * NPN;
-      const int64_t ra = pn[a];
-      const int32_t cb = pn[b];
-      int64_t lo = A.indptr[ra], hi = A.indptr[ra + 1];
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (A.indices[mid] < cb) lo = mid + 1; else hi = mid;
-      }
-      slotB[t] = (lo < A.indptr[ra + 1] && A.indices[lo] == cb) ? (int32_t)lo : -1;
-      int64_t sp = -1;
-      if (slotB[t] < 0 && A.pp_indptr != nullptr) {
-        lo = A.pp_indptr[ra];
-        hi = A.pp_indptr[ra + 1];
-        while (lo < hi) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (A.pp_indices[mid] < cb) lo = mid + 1; else hi = mid;
-        }
-        if (lo < A.pp_indptr[ra + 1] && A.pp_indices[lo] == cb) sp = lo;
-      }
-      slotP[t] = (int32_t)sp;
+      const int32_t v = ps[t];
+      slotB[t] = v >= 0 ? v : -1;
+      slotP[t] = v <= -2 ? -(v + 2) : -1;
     }
     for (int i = tid; i < D * CS; i += NT) (&colk[0][0])[i] = 0.0;
     for (int i = tid; i < W * CTP; i += NT) (&prow[0][0])[i] = 0.0;
@@ -2340,7 +2358,7 @@ template <int NP, int NC, int W, int MINB>
 void factorize_pw_dispatch(const DevMatrix& A, const DevPatchGroup& g, int64_t* status,
                            cudaStream_t s) {
   vanka_factorize_pw_kernel<NP, NC, W, MINB><<<(unsigned)g.n_patches, 32 * W, 0, s>>>(
-      A, g.n_patches, g.nodes, g.inv, g.ld, status);
+      A, g.n_patches, g.slots, g.inv, g.ld, status);
 }
 
 }  // namespace
@@ -2358,6 +2376,16 @@ void launch_sell_pack(int64_t n_pos, int R, int nc2, const int64_t* map, const d
   if (n_pos == 0) return;
   sell_pack_kernel<<<(int)std::min<int64_t>(grid_for(n_pos, 256), 4 * 148 * 8), 256, 0, s>>>(
       n_pos, R, nc2, map, data, val);
+}
+
+bool vanka_uses_slots(int np) { return np == 75 || np == 108; }
+
+void launch_patch_slots(const DevMatrix& A, const DevPatchGroup& g, int32_t* slots,
+                        cudaStream_t s) {
+  const int64_t n = g.n_patches * g.npn * g.npn;
+  if (n == 0) return;
+  patch_slots_kernel<<<(unsigned)grid_for(n, 256), 256, 0, s>>>(A, g.n_patches, g.npn, g.nodes,
+                                                               slots);
 }
 
 int64_t vanka_factorize_work(int np, int64_t n_patches) {

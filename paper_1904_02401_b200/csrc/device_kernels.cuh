@@ -49,10 +49,16 @@ struct DevPatchGroup {
   double* inv = nullptr;            // (n_patches, np, ld) column-major inverses
   int64_t y_offset = 0;             // start of this group's rows in Y
   double* work = nullptr;           // factorisation scratch, vanka_factorize_work doubles
+  const int32_t* slots = nullptr;   // (n_patches, npn, npn) operator slots (vanka_uses_slots)
 };
 
 // (nc, dofs per patch) combinations with compiled Vanka kernels
 bool vanka_supported(int nc, int np);
+// patch sizes whose factorisation kernel reads a per-patch operator-slot table
+// (launch_patch_slots, rebuilt when the sparsity pattern or the patches change)
+bool vanka_uses_slots(int np);
+void launch_patch_slots(const DevMatrix& A, const DevPatchGroup& g, int32_t* slots,
+                        cudaStream_t s);
 // factorisation scratch of a patch group in doubles (0: none needed)
 int64_t vanka_factorize_work(int np, int64_t n_patches);
 // gather A_i = R_i A R_i^T and invert (Gauss-Jordan, partial pivoting);

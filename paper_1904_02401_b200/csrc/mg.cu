@@ -112,12 +112,15 @@ struct Group {
   DevBuf<int32_t> nodes;
   DevBuf<double> inv;
   DevBuf<double> fwork;   // factorisation scratch (500 x 500 macro patches), kept
+  DevBuf<int32_t> slots;  // operator slots of the patches' node pairs (75 / 108)
+  int64_t slots_epoch = -1;   // pattern epoch the table was built for
 };
 
 struct Level {
   int64_t n_nodes = 0;
   int nc = 0;
   bool has_matrix = false;
+  int64_t pattern_epoch = 0;   // bumped whenever indptr / indices are (re)loaded
   int64_t nnzb = 0, nnz_pp = 0;
   DevBuf<int64_t> indptr, pp_indptr;
   DevBuf<int32_t> indices, pp_indices;
@@ -595,6 +598,14 @@ struct MgHandle {
         dg.n_patches = g->n_patches;
         dg.nodes = g->nodes.p;
         dg.inv = g->inv.p;
+        if (vanka_uses_slots(g->np)) {
+          if (g->slots_epoch != L.pattern_epoch) {
+            CK(g->slots.ensure((size_t)g->n_patches * g->npn * g->npn));
+            launch_patch_slots(L.mat(), dg, g->slots.p, stream);
+            g->slots_epoch = L.pattern_epoch;
+          }
+          dg.slots = g->slots.p;
+        }
         launch_vanka_factorize(L.mat(), dg, status.p, stream);
         CK(cudaGetLastError());
         int64_t st = 0;
@@ -941,6 +952,7 @@ int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nn
   L.n_nodes = n_nodes;
   L.nnzb = nnzb;
   L.nnz_pp = nnz_pp;
+  ++L.pattern_epoch;
   CKAPI(L.indptr.upload(indptr, n_nodes + 1, m->stream));
   CKAPI(L.indices.upload(indices, nnzb, m->stream));
   CKAPI(L.data.upload(data, (size_t)nnzb * nc * nc, m->stream));
@@ -993,6 +1005,7 @@ int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t n
   L.n_nodes = n_nodes;
   L.nnzb = nnzb;
   L.nnz_pp = nnz_pp;
+  ++L.pattern_epoch;
   CKAPI(L.indptr.upload(indptr, n_nodes + 1, m->stream));
   CKAPI(L.indices.upload(indices, nnzb, m->stream));
   CKAPI(L.data.alloc((size_t)nnzb * nc * nc));
