@@ -111,27 +111,62 @@ def test_live_reference_residual_and_extension(ext):
         assert np.abs(E - Er).max() <= 1e-13 * np.abs(Er).max()
 
 
+def config4_envelope():
+    """Per time step, the Newton-step and assembly counts the UNMODIFIED
+    reference itself produced on BASELINE config 4 (tests/golden/make_golden.py
+    3d_timestep): its stock run (3d_timestep.json: the completed steps of the
+    10-step run) and its run with a 16-thread patch pool on the GPU box's host
+    (3d_timestep_2steps_t16.json).  The two runs of the same reference differ
+    at t = 0.02 (18 and 17 Newton steps): the solve sits on a plateau for
+    seven steps and leaves it at a step that moves with the round-off of the
+    1e-4-accurate momentum solves.  Steps the stock run has not reached fall
+    back to the CPU oracle's 10-step record (3d_timestep_oracle.json)."""
+    runs = [load_golden("3d_timestep")[0], load_golden("3d_timestep_2steps_t16")[0]]
+    oracle = load_golden("3d_timestep_oracle")[0]
+    env = []
+    for s in range(oracle["n_steps"]):
+        recs = [r["records"][s] for r in runs if s < r["n_steps"]]
+        source = "reference"
+        if not any(s < r["n_steps"] for r in runs[:1]):
+            recs = recs + [oracle["records"][s]]
+            source = "oracle" if len(recs) == 1 else "reference + oracle"
+        env.append({"newton": sorted({r["newton_steps"][0] for r in recs}),
+                    "assemblies": sorted({r["assemblies"][0] for r in recs}),
+                    "source": source})
+    return env, runs, oracle
+
+
+def test_config4_reference_envelope_fixture():
+    """The committed reference runs: identical first step, and the stagnating
+    step t = 0.02 shows the reference's own run-to-run spread."""
+    env, runs, oracle = config4_envelope()
+    assert runs[0]["source"].startswith("reference") and runs[1]["source"].startswith("reference")
+    assert runs[1]["pool_threads"] == 16 and runs[0]["pool_threads"] == 0
+    assert env[0]["newton"] == [6] and env[0]["assemblies"] == [5]
+    assert env[1]["newton"] == [17, 18]
+    # the oracle's own 10-step record lies inside the envelope wherever the
+    # reference's stock run has got to
+    for s in range(runs[0]["n_steps"]):
+        assert oracle["records"][s]["newton_steps"][0] in env[s]["newton"]
+
+
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available(), reason="no CUDA device")
-def test_device_config4_vs_cpu_oracle():
-    """BASELINE config 4 at full size (10 steps, config-2 mesh) against the
-    CPU oracle's run (tests/golden/3d_timestep_oracle.json, made by
-    scripts/timestep_run.py --oracle).  Newton solves that stagnate along the
-    1e-8 tolerance (t=0.02 and t=0.08: 17-18 oracle steps with reassembly
-    every step) cross the tolerance at a step that moves under last-bit
-    differences of the linear solves (measured: the unblocked and the blocked
-    coarse Gauss-Jordan inverse, whose GMRES histories agree to 1e-13, give
-    17 and 19 steps at t=0.02, 17 and 15 at t=0.08); there the device must
-    converge within 20 % of the oracle's count.  Every other step must match
-    the oracle's Newton and assembly counts exactly, and the final state
-    agrees to the nonlinear tolerance."""
-    g, _ = load_golden("3d_timestep_oracle")
+def test_device_config4_vs_reference():
+    """BASELINE config 4 at full size (10 steps, config-2 mesh) on the device:
+    every step's Newton-step and assembly counts lie within the envelope of
+    the reference's own runs (exact wherever those runs agree — nine of the ten
+    steps), the first step's GMRES counts equal the reference's, and the final
+    state agrees with the 10-step record to the nonlinear tolerance."""
+    env, runs, oracle = config4_envelope()
     U, recs = W.run_timestepping(W.TIMESTEPPING["3d_timestep"], newton.LinearStack)
-    assert len(recs) == g["n_steps"]
-    for r, o in zip(recs, g["records"]):
-        n, no = r["newton_steps"][0], o["newton_steps"][0]
-        if no > 10:
-            assert abs(n - no) <= max(1, round(0.2 * no)), (r["t"], n, no)
-        else:
-            assert n == no and r["assemblies"][0] == o["assemblies"][0], (r["t"], n, no)
-    np.testing.assert_allclose(vector_checksums(U.reshape(-1)), g["U_checksums"], rtol=1e-5)
+    assert len(recs) == oracle["n_steps"]
+    for r, e in zip(recs, env):
+        n, a = r["newton_steps"][0], r["assemblies"][0]
+        assert e["newton"][0] <= n <= e["newton"][-1], (r["t"], n, e)
+        assert e["assemblies"][0] <= a <= e["assemblies"][-1], (r["t"], a, e)
+    ref0 = runs[0]["records"][0]
+    assert recs[0]["momentum_iters"] == ref0["momentum_iters"]
+    assert recs[0]["extension_iters"] == ref0["extension_iters"]
+    final = runs[0] if runs[0]["n_steps"] == oracle["n_steps"] and "U_checksums" in runs[0] else oracle
+    np.testing.assert_allclose(vector_checksums(U.reshape(-1)), final["U_checksums"], rtol=1e-5)
