@@ -25,6 +25,11 @@ constexpr int kMaxQ = 27, kMaxB = 27;
 __constant__ double cN[2][kMaxQ * kMaxB];          // N[q][b]
 __constant__ double cdN[2][kMaxQ * kMaxB * 3];     // dN[q][b][j]
 __constant__ double cW[2][kMaxQ];                  // Gauss weights
+// the same N / dN tables in global memory: the per-cell kernels stage them into
+// shared memory with coalesced loads (per-lane indexing of the constant bank
+// is serialised by the constant cache)
+__device__ double gN[2][kMaxQ * kMaxB];
+__device__ double gdN[2][kMaxQ * kMaxB * 3];
 
 template <int D>
 __device__ __forceinline__ double det(const double (&A)[D][D]) {
@@ -67,6 +72,9 @@ struct CellShared {
   double M[kMaxQ][9];               // fluid: grad v F^-1;  solid: F F^T
   double s[kMaxQ][6];               // per-q weights
   double Jinv[kMaxQ][9];
+  double N[kMaxQ * kMaxB];          // shape values N[q][b] (copy of the constant table:
+                                    // the kernels index it per lane, which the constant
+                                    // cache serialises)
   int slot[kMaxB * kMaxB];
   int bad;
 };
@@ -82,6 +90,11 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
   const int64_t cell = cells[blockIdx.x];
   const int32_t* cn = a.cell_nodes + cell * NB;
   if (tid == 0) sh.bad = 0;
+  // shape tables into shared memory: N for the whole kernel, dN in the space
+  // of S until the physical gradients G are formed
+  double* const dNs = &sh.S[0][0][0];
+  for (int t = tid; t < NQ * NB; t += blockDim.x) sh.N[t] = gN[D == 3][t];
+  for (int t = tid; t < NQ * NB * 3; t += blockDim.x) dNs[t] = gdN[D == 3][t];
   for (int t = tid; t < NB * D; t += blockDim.x) sh.X[t / D][t % D] = a.coords[(int64_t)cn[t / D] * D + t % D];
   for (int t = tid; t < NB * NF; t += blockDim.x) {
     const int b = t / NF, f = t - b * NF;
@@ -110,7 +123,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
 #pragma unroll
       for (int j = 0; j < D; ++j) {
         double acc = 0.0;
-        for (int b = 0; b < NB; ++b) acc += sh.X[b][i] * cdN[D == 3][(q * NB + b) * 3 + j];
+        for (int b = 0; b < NB; ++b) acc += sh.X[b][i] * dNs[(q * NB + b) * 3 + j];
         J[i][j] = acc;
       }
     const double dt = det<D>(J);
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
     for (int i = 0; i < D; ++i) {
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < D; ++j) acc += cdN[D == 3][(q * NB + b) * 3 + j] * sh.Jinv[q][j * D + i];
+      for (int j = 0; j < D; ++j) acc += dNs[(q * NB + b) * 3 + j] * sh.Jinv[q][j * D + i];
       sh.G[q][b][i] = acc;
     }
   }
@@ -146,7 +159,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
       for (int j = 0; j < D; ++j) gv[i][j] = gu[i][j] = gvp[i][j] = gup[i][j] = 0.0;
     }
     for (int b = 0; b < NB; ++b) {
-      const double nb = cN[D == 3][q * NB + b];
+      const double nb = sh.N[q * NB + b];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         v[i] += nb * sh.U[b][1 + i];
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
       for (int j = 0; j < NC; ++j) blk[i][j] = 0.0;
     double diag = 0.0;
     for (int q = 0; q < NQ; ++q) {
-      const double nb = cN[D == 3][q * NB + b], na = cN[D == 3][q * NB + c];
+      const double nb = sh.N[q * NB + b], na = sh.N[q * NB + c];
       if constexpr (KIND == 0) {
         double gkg = 0.0;
 #pragma unroll
@@ -852,7 +865,11 @@ int set_assembly_tables(const double* N, const double* dN, const double* w, int 
           cudaSuccess ||
       cudaMemcpyToSymbol(cdN, tdN, sizeof(double) * nq * nb * 3,
                          o * sizeof(double) * kMaxQ * kMaxB * 3) != cudaSuccess ||
-      cudaMemcpyToSymbol(cW, tW, sizeof(double) * nq, o * sizeof(double) * kMaxQ) != cudaSuccess)
+      cudaMemcpyToSymbol(cW, tW, sizeof(double) * nq, o * sizeof(double) * kMaxQ) != cudaSuccess ||
+      cudaMemcpyToSymbol(gN, tN, sizeof(double) * nq * nb, o * sizeof(double) * kMaxQ * kMaxB) !=
+          cudaSuccess ||
+      cudaMemcpyToSymbol(gdN, tdN, sizeof(double) * nq * nb * 3,
+                         o * sizeof(double) * kMaxQ * kMaxB * 3) != cudaSuccess)
     return 3;
   loaded[bank] = true;
   return 0;
