@@ -101,18 +101,9 @@ __global__ void __launch_bounds__(256) assemble_cells_kernel(AsmArgs a, const in
     sh.U[b][f] = a.U[(int64_t)cn[b] * NF + f];
     sh.Up[b][f] = a.Up[(int64_t)cn[b] * NF + f];
   }
-  // block slots of every (row b, column a) node pair
-  for (int t = tid; t < NB * NB; t += blockDim.x) {
-    const int b = t / NB, c = t - b * NB;
-    const int64_t row = cn[b];
-    const int32_t col = cn[c];
-    int64_t lo = a.indptr[row], hi = a.indptr[row + 1];
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (a.indices[mid] < col) lo = mid + 1; else hi = mid;
-    }
-    sh.slot[t] = (int)lo;
-  }
+  // block slots of every (row b, column a) node pair (table built once per pattern)
+  for (int t = tid; t < NB * NB; t += blockDim.x)
+    sh.slot[t] = a.cell_slots[cell * (NB * NB) + t];
   __syncthreads();
   // geometry: J = sum_b X_b (x) dN_b, its inverse and weighted determinant
   if (tid < NQ) {

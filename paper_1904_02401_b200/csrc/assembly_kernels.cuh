@@ -10,8 +10,7 @@ struct AsmArgs {
   const double* coords = nullptr;        // (n_nodes, d)
   const double* U = nullptr;             // (n_nodes, 1 + 2d) current state
   const double* Up = nullptr;            // previous time step
-  const int64_t* indptr = nullptr;       // cell-stencil block pattern
-  const int32_t* indices = nullptr;
+  const int32_t* cell_slots = nullptr;   // (n_cells, 3^d, 3^d) block slot of (row node, column node)
   double* data = nullptr;                // (nnzb, d+1, d+1) output, accumulated
   int64_t* status = nullptr;             // 1 + first inverted cell
   double rho_f = 0, mu_f = 0, rho_s = 0, mu_s = 0, lam_s = 0, k = 0, theta = 0;

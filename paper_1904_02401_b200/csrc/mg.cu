@@ -141,6 +141,8 @@ struct Level {
   bool has_asm = false;
   int dim = 0;
   DevBuf<int32_t> asm_cell_nodes, asm_group_cells;
+  DevBuf<int32_t> asm_cell_slots;    // (n_cells, nb, nb) block slots of the cells' node pairs
+  int64_t asm_n_cells = 0, asm_slots_epoch = -1;
   DevBuf<double> asm_coords, asm_U, asm_Up, res_out, asm_extra_vals;
   DevBuf<int64_t> asm_extra_slots;
   // do-nothing outflow facets assembled on the device
@@ -1049,6 +1051,8 @@ int alefsi_mg_asm_setup(alefsi_mg h, int32_t level, int32_t dim, int64_t n_cells
   const int nb = dim == 3 ? 27 : 9;
   L.dim = dim;
   CKAPI(L.asm_cell_nodes.upload(cell_nodes, (size_t)n_cells * nb, m->stream));
+  L.asm_n_cells = n_cells;
+  L.asm_slots_epoch = -1;
   CKAPI(L.asm_coords.upload(coords, (size_t)L.n_nodes * dim, m->stream));
   L.asm_group_ptr.assign(group_ptr, group_ptr + n_groups + 1);
   L.asm_group_kind.assign(group_kind, group_kind + n_groups);
@@ -1103,13 +1107,23 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
   if (L.nnz_pp > 0) CKAPI(cudaMemsetAsync(L.pp_data.p, 0, sizeof(double) * L.nnz_pp, s));
   CKAPI(cudaMemsetAsync(m->status.p, 0, sizeof(int64_t), s));
   L.sell_dirty = true;
+  if (L.asm_slots_epoch != L.pattern_epoch) {
+    // block slots of every cell's node pairs, once per sparsity pattern
+    const int nb = L.dim == 3 ? 27 : 9;
+    CKAPI(L.asm_cell_slots.ensure((size_t)L.asm_n_cells * nb * nb));
+    alefsi::DevPatchGroup cg;
+    cg.npn = nb;
+    cg.n_patches = L.asm_n_cells;
+    cg.nodes = L.asm_cell_nodes.p;
+    alefsi::launch_patch_slots(L.mat(), cg, L.asm_cell_slots.p, s);
+    L.asm_slots_epoch = L.pattern_epoch;
+  }
   alefsi::AsmArgs a;
   a.cell_nodes = L.asm_cell_nodes.p;
+  a.cell_slots = L.asm_cell_slots.p;
   a.coords = L.asm_coords.p;
   a.U = L.asm_U.p;
   a.Up = L.asm_Up.p;
-  a.indptr = L.indptr.p;
-  a.indices = L.indices.p;
   a.data = L.data.p;
   a.status = m->status.p;
   a.rho_f = params[0];
