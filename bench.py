@@ -286,7 +286,10 @@ def run_ours(args, rank, world):
     for l, lvl in enumerate(prob.levels):
         solver.asm_momentum(l, lvl, prob.mats, wl.dt, wl.theta, prob.restrict_state(U, l),
                             prob.restrict_state(Up, l))
-    torch.cuda.synchronize()
+    # the launch stream only: the coarse inverse started by the level-0
+    # assembly keeps running on the library's side stream and is joined by
+    # factorize()
+    torch.cuda.current_stream().synchronize()
     t1 = time.perf_counter()
     solver.factorize()
     torch.cuda.synchronize()

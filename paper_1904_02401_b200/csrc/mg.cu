@@ -306,6 +306,10 @@ struct MgHandle {
   cudaStream_t side_stream = nullptr;
   cudaEvent_t side_in = nullptr, side_out = nullptr;
   bool factorized = false;
+  // the coarse inverse of the freshly assembled level 0 is already running
+  // on the side stream (started by alefsi_mg_asm_momentum(level 0), so that
+  // it overlaps the assembly of the finer levels)
+  bool coarse_inflight = false;
   // graph-captured V-cycle (fixed in/out buffers)
   bool use_graph = false;
   bool graph_valid = false;
@@ -558,6 +562,12 @@ struct MgHandle {
     return ALEFSI_OK;
   }
 
+  // level 0's operator is about to change: let an early-started inverse drain
+  void cancel_coarse_inflight() {
+    if (coarse_inflight && side_stream) cudaStreamSynchronize(side_stream);
+    coarse_inflight = false;
+  }
+
   int finish_coarse_inverse() {
     CK(cudaStreamWaitEvent(stream, side_out, 0));
     int64_t st = 0;
@@ -570,7 +580,8 @@ struct MgHandle {
   int factorize() {
     const std::vector<const void*> before = graph_buffers();
     for (auto& L : lv) refresh_sell(L, stream);
-    int rc = start_coarse_inverse();
+    int rc = coarse_inflight ? ALEFSI_OK : start_coarse_inverse();
+    coarse_inflight = false;
     if (rc) {
       if (side_stream) cudaStreamSynchronize(side_stream);
       return rc;
@@ -954,6 +965,7 @@ int alefsi_mg_set_matrix(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t nn
   L.n_nodes = n_nodes;
   L.nnzb = nnzb;
   L.nnz_pp = nnz_pp;
+  if (level == 0) m->cancel_coarse_inflight();
   ++L.pattern_epoch;
   CKAPI(L.indptr.upload(indptr, n_nodes + 1, m->stream));
   CKAPI(L.indices.upload(indices, nnzb, m->stream));
@@ -1007,6 +1019,7 @@ int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t n
   L.n_nodes = n_nodes;
   L.nnzb = nnzb;
   L.nnz_pp = nnz_pp;
+  if (level == 0) m->cancel_coarse_inflight();
   ++L.pattern_epoch;
   CKAPI(L.indptr.upload(indptr, n_nodes + 1, m->stream));
   CKAPI(L.indices.upload(indices, nnzb, m->stream));
@@ -1099,6 +1112,7 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
   if (rc) return rc;
   auto& L = m->lv[level];
   if (!L.has_asm) return fail(ALEFSI_ERR_STATE, "asm_setup missing");
+  if (level == 0) m->cancel_coarse_inflight();
   const int nc = m->nc, nf = 1 + 2 * L.dim;
   cudaStream_t s = m->stream;
   CKAPI(cudaMemcpyAsync(L.asm_U.p, U, sizeof(double) * L.n_nodes * nf, cudaMemcpyHostToDevice, s));
@@ -1177,6 +1191,16 @@ int alefsi_mg_asm_momentum(alefsi_mg h, int32_t level, const double* params, con
                                          std::to_string(st - 1));
   // operator values change in place: the V-cycle graph (pointers only) stays
   m->factorized = false;
+  if (level == 0 && m->n_levels > 1) {
+    // the coarse inverse is a serial chain of ~n/16 panel steps: start it now,
+    // under the assembly of the finer levels (alefsi_mg_factorize joins it)
+    rc = m->start_coarse_inverse();
+    if (rc) {
+      if (m->side_stream) cudaStreamSynchronize(m->side_stream);
+      return rc;
+    }
+    m->coarse_inflight = true;
+  }
   return ALEFSI_OK;
   ALEFSI_TRY_END
 }
