@@ -130,7 +130,10 @@ int alefsi_mg_set_pattern(alefsi_mg h, int32_t level, int64_t n_nodes, int64_t n
  * asm_momentum: params = {rho_f, mu_f, rho_s, mu_s, lam_s, k, theta}; U and
  * U_prev host (n_nodes, 1+2dim); extra = host-reduced outflow-facet blocks
  * (unique slots; pass n_extra = 0 once asm_outflow has been called for the
- * level).  The matrix must be re-factorised afterwards.
+ * level).  The matrix must be re-factorised afterwards.  Assembling level 0
+ * also starts that level's dense inverse on a side stream, so that it runs
+ * under the assembly of the finer levels; alefsi_mg_factorize joins it (any
+ * later change of level 0 before the factorisation discards it).
  * asm_outflow (once per level): the do-nothing outflow facets
  * (model._outflow_blocks, reference model.py:363-375) for assembly on the
  * device: owner-cell nodes conn (n_facets, 3^dim) and cell ids, facet
