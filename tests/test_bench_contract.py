@@ -89,3 +89,19 @@ def test_ref_arm_state_rhs_and_threaded_setup_are_exact():
     assert st.iterations == g["iterations"]
     np.testing.assert_allclose(st.residuals, g["residuals"], rtol=1e-10)
     assert "paper_1904_02401_b200" not in ref_arm.ref().__file__
+
+
+def test_clock_sampler_summary_contract():
+    """The `clocks` object of the JSON line: keys present with and without a
+    device (no samples here), and the nvidia-smi line parser (median SM clock,
+    max clock, throttle reasons that were active in any sample)."""
+    with bench.ClockSampler(0) as clk:
+        pass
+    s = clk.summary()
+    assert set(s) >= {"sm_mhz", "sm_max_mhz", "reasons", "samples", "sampler"}
+    clk.lines = ["1500, 1965, Not Active, Not Active, Not Active, Active",
+                 "1700, 1965, Not Active, Not Active, Not Active, Not Active",
+                 "1600, 1965, Not Active, Not Active, Not Active, Active"]
+    s = clk.summary()
+    assert s["sm_mhz"] == 1600 and s["sm_max_mhz"] == 1965 and s["samples"] == 3
+    assert s["reasons"] == ["sw_power_cap"]
