@@ -114,14 +114,19 @@ def test_live_reference_residual_and_extension(ext):
 def config4_envelope():
     """Per time step, the Newton-step and assembly counts the UNMODIFIED
     reference itself produced on BASELINE config 4 (tests/golden/make_golden.py
-    3d_timestep): its stock run (3d_timestep.json: the completed steps of the
-    10-step run) and its run with a 16-thread patch pool on the GPU box's host
-    (3d_timestep_2steps_t16.json).  The two runs of the same reference differ
+    3d_timestep): its stock 10-step run (3d_timestep.json, 4.9 h in the build
+    container) and its run with a 16-thread patch pool on the GPU box's host
+    (3d_timestep_2steps_t16.json, or the longer 3d_timestep_t16.json when
+    present).  The two runs of the same reference differ
     at t = 0.02 (18 and 17 Newton steps): the solve sits on a plateau for
     seven steps and leaves it at a step that moves with the round-off of the
     1e-4-accurate momentum solves.  Steps the stock run has not reached fall
     back to the CPU oracle's 10-step record (3d_timestep_oracle.json)."""
-    runs = [load_golden("3d_timestep")[0], load_golden("3d_timestep_2steps_t16")[0]]
+    import os
+    from conftest import GOLDEN
+    second = "3d_timestep_t16" if os.path.exists(os.path.join(GOLDEN, "3d_timestep_t16.json")) \
+        else "3d_timestep_2steps_t16"
+    runs = [load_golden("3d_timestep")[0], load_golden(second)[0]]
     oracle = load_golden("3d_timestep_oracle")[0]
     env = []
     for s in range(oracle["n_steps"]):
@@ -156,8 +161,10 @@ def test_device_config4_vs_reference():
     """BASELINE config 4 at full size (10 steps, config-2 mesh) on the device:
     every step's Newton-step and assembly counts lie within the envelope of
     the reference's own runs (exact wherever those runs agree — nine of the ten
-    steps), the first step's GMRES counts equal the reference's, and the final
-    state agrees with the 10-step record to the nonlinear tolerance."""
+    steps), the GMRES counts of every solve equal the reference's on the
+    non-stagnating steps, and the final state agrees with the reference's
+    10-step record to 1e-6 (observed 2e-7; the Newton tolerance is 1e-8 of
+    the initial residual)."""
     env, runs, oracle = config4_envelope()
     U, recs = W.run_timestepping(W.TIMESTEPPING["3d_timestep"], newton.LinearStack)
     assert len(recs) == oracle["n_steps"]
@@ -165,8 +172,15 @@ def test_device_config4_vs_reference():
         n, a = r["newton_steps"][0], r["assemblies"][0]
         assert e["newton"][0] <= n <= e["newton"][-1], (r["t"], n, e)
         assert e["assemblies"][0] <= a <= e["assemblies"][-1], (r["t"], a, e)
-    ref0 = runs[0]["records"][0]
-    assert recs[0]["momentum_iters"] == ref0["momentum_iters"]
-    assert recs[0]["extension_iters"] == ref0["extension_iters"]
-    final = runs[0] if runs[0]["n_steps"] == oracle["n_steps"] and "U_checksums" in runs[0] else oracle
-    np.testing.assert_allclose(vector_checksums(U.reshape(-1)), final["U_checksums"], rtol=1e-5)
+    # GMRES counts of every momentum and extension solve equal the reference's
+    # on the steps that do not stagnate (at most 10 Newton steps: eight of ten)
+    stock = runs[0]
+    checked = 0
+    for r, g in zip(recs, stock["records"]):
+        if g["newton_steps"][0] <= 10:
+            assert r["momentum_iters"] == g["momentum_iters"], r["t"]
+            assert r["extension_iters"] == g["extension_iters"], r["t"]
+            checked += 1
+    assert checked >= min(8, stock["n_steps"] - 2)
+    final = stock if stock["n_steps"] == oracle["n_steps"] and "U_checksums" in stock else oracle
+    np.testing.assert_allclose(vector_checksums(U.reshape(-1)), final["U_checksums"], rtol=1e-6)
