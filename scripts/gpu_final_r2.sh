@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2, final evidence: parity suite, bench lines of every workload on the
 # final kernels (clock record per line), launch list of the default bench.
-OUT=${OUT:-r2w}
+OUT=${OUT:-r2x}
 mkdir -p gpurun_out/$OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > gpurun_out/$OUT/smi.txt
 timeout 1800 python -m pytest tests -m gpu -q -x --timeout 900 -rs --durations=10 > gpurun_out/$OUT/pytest.log 2>&1
