@@ -426,6 +426,7 @@ def run_ours(args, rank, world):
                      "avg_launch_ms": avg_ms, "share_of_step": ms / ms_prof,
                      "peak_source": peak_src},
         "vanka_sweeps_per_s": 1e3 / ms_sweep,
+        "vanka_sweeps_timed": nsw,      # standalone finest-level sweep benchmark (--sweeps)
         "vanka_sweep_ms": ms_sweep,
         "spmv_ms": ms_spmv, "spmv_gbs": kb["spmv"] / (ms_spmv * 1e-3) / 1e9,
         "vanka_apply_gbs": kb["vanka_apply"] / (prof[("vanka_apply", True)][1] /
